@@ -1,0 +1,177 @@
+/*
+ * pensieve_b200.h — C-ABI of the B200-native Pensieve hot path.
+ *
+ * Plain pointers and sizes only (no torch / C++ types).  Every entry point names the
+ * reference interface it replaces (paths relative to /root/reference/proj).  Device
+ * pointers are caller-owned; `stream` is a cudaStream_t passed as void* (NULL = legacy
+ * default stream).  Calls are asynchronous on `stream` unless stated otherwise.
+ *
+ * Errors: every function returns pb_status; the codes map 1:1 onto the reference's
+ * exception classes (include/kvsim/errors.hpp).  Validation happens before any mutation
+ * or launch, exactly like the reference (which validates, then throws without side
+ * effects).  pb_last_error() returns the message of the calling thread's last failure.
+ */
+#ifndef PENSIEVE_B200_H
+#define PENSIEVE_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum pb_status {
+    PB_OK = 0,
+    PB_ERR_DIMENSION_MISMATCH = 1,        /* kvsim::DimensionMismatch  errors.hpp:76-79 */
+    PB_ERR_NUMERIC = 2,                   /* kvsim::NumericError       errors.hpp:82-85 */
+    PB_ERR_ERROR = 3,                     /* kvsim::Error (base)       errors.hpp:12-15 */
+    PB_ERR_INSUFFICIENT_DEVICE_MEMORY = 4,/* errors.hpp:23-26 */
+    PB_ERR_INSUFFICIENT_HOST_MEMORY = 5,  /* errors.hpp:29-32 */
+    PB_ERR_INVALID_CHUNK_STATE = 6,       /* errors.hpp:41-44 */
+    PB_ERR_UNKNOWN_CONVERSATION = 7,      /* errors.hpp:34-37 */
+    PB_ERR_CONFIG = 8,                    /* kvsim::ConfigError */
+    PB_ERR_NOT_ENOUGH_EVICTABLE = 9,      /* kvsim::NotEnoughEvictable */
+    PB_ERR_TRACE_MISSING = 10,            /* kvsim::TraceMissing */
+    PB_ERR_CANNOT_SUSPEND_ALL = 11,       /* kvsim::CannotSuspendAll */
+    PB_ERR_CUDA = 20,                     /* CUDA runtime/driver failure (no ref analogue) */
+    PB_ERR_UNSUPPORTED = 21               /* shape outside what the kernels were built for */
+} pb_status;
+
+typedef enum pb_dtype { PB_F32 = 0, PB_BF16 = 1 } pb_dtype;
+
+const char* pb_last_error(void);
+const char* pb_version(void);
+/* Number of kernel launches issued by this process so far (all pb_* kernels). */
+uint64_t pb_launch_count(void);
+
+/* ===================================================================== attention
+ *
+ * Layouts (identical to the reference):
+ *   q, out : [total_tokens][n_head][head_size]              (RaggedQueryBatch::q,
+ *                                                            include/kvsim/attention.hpp:53-65)
+ *   pages  : [n_slots][chunk_size][n_kv_head][head_size]   (PagedKvStore keys / values,
+ *                                                            include/kvsim/attention.hpp:33-49,
+ *                                                            src/attention.cpp:60-71)
+ *   spans  : SubRequest{query_start, query_len, context_len, causal_offset, block_table}
+ *            (include/kvsim/batch.hpp:17-24); block tables as CSR: the slots of span s are
+ *            block_tables[block_table_offsets[s] .. block_table_offsets[s+1]).
+ * Semantics: query token i of span s attends to context positions [0, causal_offset+i];
+ * query head h reads kv head h / (n_head / n_kv_head); scores are dot / scale
+ * (src/attention.cpp:73-132).
+ * dtype PB_F32 is the fp32 validation mode (fp32 SIMT, 1e-5 parity); PB_BF16 is the
+ * production mode (bf16 storage, fp32 accumulation; tcgen05 tiles for multi-token spans,
+ * split-KV SIMT for single-token spans).
+ */
+typedef struct pb_attn_shape {
+    int32_t n_head;
+    int32_t n_kv_head;
+    int32_t head_size;
+    int32_t chunk_size; /* tokens per page (= the reference's chunk_size) */
+    int32_t n_slots;    /* pages in the pool */
+    int32_t dtype;      /* pb_dtype of q, pages and out */
+    double scale;       /* scores are divided by this (RaggedQueryBatch::scale) */
+} pb_attn_shape;
+
+typedef struct pb_attn_plan pb_attn_plan;
+
+enum {
+    PB_PLAN_SINGLE_TOKEN = 1, /* single_token_attention contract: every query_len == 1 */
+    PB_PLAN_FORCE_SIMT = 2,   /* route every span through the SIMT kernel (diagnostics) */
+    PB_PLAN_NO_SPLIT = 4      /* never split a decode span's context across CTAs */
+};
+
+/* Validates the batch exactly as check_batch (src/attention.cpp:23-48, minus the q
+ * finiteness scan, which needs the data: see pb_attn_check_numerics) and builds the
+ * host-side work list (prefill tiles + decode split units, heavy first).  The plan is
+ * reusable across layers and calls.  Replaces the per-call
+ * bookkeeping inside paged_multi_token_attention / single_token_attention. */
+pb_status pb_attn_plan_create(const pb_attn_shape* shape, int32_t n_spans,
+                              const int64_t* query_start, const int64_t* query_len,
+                              const int64_t* context_len, const int64_t* causal_offset,
+                              const int32_t* block_tables, const int64_t* block_table_offsets,
+                              int64_t total_tokens, int32_t flags, pb_attn_plan** out);
+/* Copies the plan's descriptors to the device on `stream` (first call allocates). */
+pb_status pb_attn_plan_upload(pb_attn_plan* plan, void* stream);
+/* Device workspace bytes pb_attn_run needs (split-KV partials + tile counters). */
+size_t pb_attn_plan_workspace_bytes(const pb_attn_plan* plan);
+/* Plan statistics: out[0] prefill tiles, [1] decode units, [2] split spans,
+ * [3] algorithmic flops (4*n_head*d*sum allowed), [4] algorithmic bytes, [5] total tokens,
+ * [6] SIMT tiles, [7] query rows covered by the work list (must equal tokens*n_head) */
+void pb_attn_plan_stats(const pb_attn_plan* plan, double* out8);
+/* The fused ragged paged attention launch(es) for one layer.  q, pages, out, workspace are
+ * device pointers; the plan must have been uploaded.  Replaces
+ * paged_multi_token_attention (src/attention.cpp:73-132) and single_token_attention
+ * (:134-188) on the device. */
+pb_status pb_attn_run(pb_attn_plan* plan, const void* q, const void* k_pages,
+                      const void* v_pages, void* out, void* workspace, void* stream);
+/* Optional device-side restatement of the reference's NumericError checks: q must be
+ * finite (src/attention.cpp:30) and k_row[0] of every attended position must be finite
+ * (:100-101).  Writes 0 / PB_ERR_NUMERIC into *d_flag (device int32). */
+pb_status pb_attn_check_numerics(pb_attn_plan* plan, const void* q, const void* k_pages,
+                                 int32_t* d_flag, void* stream);
+void pb_attn_plan_destroy(pb_attn_plan* plan);
+
+/* Host-buffer, synchronous mirrors of the reference's value-semantics API
+ * (include/kvsim/attention.hpp:71-77).  q/keys/values/out are HOST fp32 arrays with the
+ * reference layouts; with shape->dtype == PB_BF16 they are rounded to bf16 on upload and
+ * the bf16 result is widened back.  Error behaviour matches the reference, including
+ * NumericError for non-finite q / k_row[0]. */
+pb_status pb_paged_multi_token_attention(const pb_attn_shape* shape, int32_t n_spans,
+                                         const int64_t* query_start, const int64_t* query_len,
+                                         const int64_t* context_len,
+                                         const int64_t* causal_offset,
+                                         const int32_t* block_tables,
+                                         const int64_t* block_table_offsets,
+                                         const float* q, int64_t total_tokens,
+                                         const float* keys, const float* values, float* out);
+pb_status pb_single_token_attention(const pb_attn_shape* shape, int32_t n_spans,
+                                    const int64_t* query_start, const int64_t* query_len,
+                                    const int64_t* context_len, const int64_t* causal_offset,
+                                    const int32_t* block_tables,
+                                    const int64_t* block_table_offsets, const float* q,
+                                    int64_t total_tokens, const float* keys,
+                                    const float* values, float* out);
+
+/* ===================================================================== KV pages
+ * A page is page_bytes contiguous bytes (chunk_size * n_kv_head * head_size elements) at
+ * pool + slot * page_bytes: PagedKvStore::key_row addressing (src/attention.cpp:60-71).
+ * Slot lists are DEVICE int32 arrays.  The reference moves no bytes; these
+ * are the copies its bookkeeping implies (PagedKvCache::apply_evictions / restore,
+ * src/paged_kv_cache.cpp:129-197). */
+
+/* staging[i] = pool[slots[i]] for i < n, for n_layers layers: the pool of layer l starts at
+ * pool + l * layer_stride; staging is [i][l] (page_bytes each) when layer_major == 0 and
+ * [l][i] when layer_major == 1. */
+pb_status pb_kv_gather_pages(const void* pool, int64_t layer_stride, int32_t n_layers,
+                             int64_t page_bytes, const int32_t* d_slots, int64_t n,
+                             void* staging, int32_t layer_major, void* stream);
+/* pool[slots[i]] = staging[i] (inverse of gather, same layouts). */
+pb_status pb_kv_scatter_pages(const void* staging, int64_t layer_stride, int32_t n_layers,
+                              int64_t page_bytes, const int32_t* d_slots, int64_t n,
+                              void* pool, int32_t layer_major, void* stream);
+/* Paged K/V append (the write loop of qkv_project, src/attention.cpp:315-327): row i
+ * (n_kv_head*head_size elements of `dtype`) goes to slot block_table[(start_pos+i)/chunk],
+ * row (start_pos+i)%chunk, for i < n_rows, one span per entry of the CSR arrays.
+ * k_rows/v_rows are [sum rows][n_kv*hs]; span s covers rows row_start[s]..+n_rows[s].
+ * Out-of-range positions/slots are rejected on the host from the HOST copies of the
+ * arrays (h_*) before the launch; d_* are the device copies the kernel reads. */
+pb_status pb_kv_append(const pb_attn_shape* shape, int32_t n_spans, const int64_t* h_row_start,
+                       const int64_t* h_n_rows, const int64_t* h_start_pos,
+                       const int32_t* h_block_tables, const int64_t* h_bt_offsets,
+                       const int64_t* d_row_start, const int64_t* d_n_rows,
+                       const int64_t* d_start_pos, const int32_t* d_block_tables,
+                       const int64_t* d_bt_offsets, const void* k_rows, const void* v_rows,
+                       void* k_pages, void* v_pages, void* stream);
+
+/* Deterministic synthetic fill: dst[i] = dtype(float(2*u01(draw first_draw+i) - 1)) where
+ * draw j is the j-th (0-based) output of SplitMix64{seed} (src/workload.cpp:30-40).
+ * Counter-based, so a GPU fill equals the sequential CPU stream bit for bit. */
+pb_status pb_fill_splitmix_unit(void* dst, int32_t dtype, int64_t n, uint64_t seed,
+                                uint64_t first_draw, void* stream);
+
+#ifdef __cplusplus
+} /* extern "C" */
+#endif
+
+#endif /* PENSIEVE_B200_H */

@@ -1,0 +1,370 @@
+// Host side of the attention C-ABI: batch validation (the reference's check_batch), the
+// work-list builder, descriptor upload and the per-layer launch.
+//
+// The plan is the B200 analogue of the "auxiliary data computed on the CPU and reused
+// across layers" of PAPER.md:967-970: spans, the block-table CSR and the work list are
+// built once per batch, uploaded once, and every layer's pb_attn_run reuses them.
+#include "attn_internal.hpp"
+#include "pb_common.hpp"
+#include "sm100_attn.hpp"
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+namespace pb {
+void launch_attn_simt(const AttnParams& p, int dtype, int n_items, cudaStream_t stream);
+void launch_check_numerics(const AttnParams& p, int dtype, int64_t q_elems, int32_t* d_flag,
+                           cudaStream_t stream);
+} // namespace pb
+
+using namespace pb;
+
+struct pb_attn_plan {
+    pb_attn_shape shape{};
+    int32_t flags = 0;
+    int32_t group = 1;
+    int64_t total_tokens = 0;
+    std::vector<SpanDev> spans;
+    std::vector<int32_t> bt;
+    std::vector<WorkItem> simt_items;
+    std::vector<WorkItem> tc_items; // prefill tiles + decode units for the sm_100a kernel
+    int32_t n_groups = 0;
+    int32_t n_parts = 0;
+    int32_t n_prefill = 0, n_decode = 0, n_split_spans = 0;
+    double flops = 0, bytes = 0;
+    // device copies: [spans | block tables | simt items | tc items]
+    void* d_buf = nullptr;
+    size_t d_bytes = 0;
+    size_t off_bt = 0, off_simt = 0, off_tc = 0;
+    bool uploaded = false;
+    void* last_workspace = nullptr;
+    Sm100Cache sm100;
+};
+
+namespace {
+
+size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int dtype_bytes(int dtype) { return dtype == PB_F32 ? 4 : 2; }
+
+// check_batch, /root/reference/proj/src/attention.cpp:23-48, in the reference's order.
+// q (host) may be null: the finiteness scan then moves to pb_attn_check_numerics.
+void validate(const pb_attn_shape& s, int32_t n_spans, const int64_t* qs, const int64_t* ql,
+              const int64_t* cl, const int64_t* co, const int32_t* bt, const int64_t* bt_off,
+              int64_t total_tokens, const float* q_host) {
+    require(s.n_head > 0 && s.head_size > 0, "batch head shape must be positive");
+    require(s.n_kv_head > 0, "store/batch head_size mismatch");
+    require(s.n_head % s.n_kv_head == 0, "n_head must be a multiple of the store's n_kv_head");
+    require(s.scale > 0, "scale must be positive");
+    if (s.chunk_size < 1) fail(PB_ERR_CONFIG, "chunk_size must be >= 1");
+    if (s.n_slots < 0) fail(PB_ERR_CONFIG, "n_slots must be >= 0");
+    if (s.dtype != PB_F32 && s.dtype != PB_BF16) fail(PB_ERR_UNSUPPORTED, "dtype must be f32 or bf16");
+    if (q_host) {
+        const int64_t n = total_tokens * s.n_head * s.head_size;
+        for (int64_t i = 0; i < n; ++i)
+            if (!std::isfinite(q_host[i])) fail(PB_ERR_NUMERIC, "query contains non-finite values");
+    }
+    require(n_spans >= 0, "negative span count");
+    int64_t expect = 0;
+    for (int32_t i = 0; i < n_spans; ++i) {
+        require(ql[i] >= 0, "negative query span");
+        require(qs[i] == expect, "sub-request spans must tile the batch");
+        require(cl[i] == co[i] + ql[i], "context_len must equal causal_offset + query_len");
+        require(co[i] >= 0, "negative causal offset");
+        const int64_t need = (cl[i] + s.chunk_size - 1) / s.chunk_size;
+        require(bt_off[i + 1] - bt_off[i] == need,
+                "block table must cover exactly ceil(context/chunk_size) slots");
+        for (int64_t j = bt_off[i]; j < bt_off[i + 1]; ++j)
+            if (bt[j] < 0 || bt[j] >= s.n_slots)
+                fail(PB_ERR_ERROR, "block table references out-of-range slot " + std::to_string(bt[j]));
+        expect += ql[i];
+    }
+    require(expect == total_tokens, "sub-request spans must tile the batch");
+    if (total_tokens > INT32_MAX / 2) fail(PB_ERR_UNSUPPORTED, "too many query tokens");
+    for (int32_t i = 0; i < n_spans; ++i)
+        if (cl[i] > INT32_MAX / 2) fail(PB_ERR_UNSUPPORTED, "context too long");
+}
+
+// Decode spans longer than this many pages are split across CTAs (split-KV); partial
+// results are merged by the last-arriving split inside the same launch.
+constexpr int kDecodeSplitPages = 64;
+
+void build_work(pb_attn_plan& P) {
+    const pb_attn_shape& s = P.shape;
+    const int g = P.group;
+    const bool tc = (P.flags & PB_PLAN_FORCE_SIMT) == 0 && s.dtype == PB_BF16 &&
+                    sm100_supports(s.head_size, s.chunk_size, g);
+    // SIMT tiles: blocks of tokens, ~16 rows per warp-pass
+    const int simt_tokens = std::max(1, 32 / g);
+    const int tc_tokens = tc ? sm100_tile_tokens(g) : 0;
+    std::vector<std::pair<double, WorkItem>> tc_list;
+    for (int32_t si = 0; si < static_cast<int32_t>(P.spans.size()); ++si) {
+        const SpanDev& sp = P.spans[si];
+        if (sp.query_len == 0) continue;
+        for (int kvh = 0; kvh < s.n_kv_head; ++kvh) {
+            if (!tc) {
+                for (int t0 = 0; t0 < sp.query_len; t0 += simt_tokens) {
+                    WorkItem w{};
+                    w.span = si;
+                    w.kvh = kvh;
+                    w.type = kWorkSimt;
+                    w.t0 = t0;
+                    w.nt = std::min(simt_tokens, sp.query_len - t0);
+                    w.group = -1;
+                    P.simt_items.push_back(w);
+                }
+            } else if (sp.query_len >= 2) {
+                for (int t0 = 0; t0 < sp.query_len; t0 += tc_tokens) {
+                    WorkItem w{};
+                    w.span = si;
+                    w.kvh = kvh;
+                    w.type = kWorkPrefill;
+                    w.t0 = t0;
+                    w.nt = std::min(tc_tokens, sp.query_len - t0);
+                    w.group = -1;
+                    const double kv = sp.causal_offset + w.t0 + w.nt;
+                    tc_list.push_back({kv * 4.0, w}); // tensor tile ~ 4x a decode page pass
+                    ++P.n_prefill;
+                }
+            } else {
+                const int pages = sp.n_pages;
+                const int n_parts = (P.flags & PB_PLAN_NO_SPLIT)
+                                        ? 1
+                                        : std::max(1, (pages + kDecodeSplitPages - 1) / kDecodeSplitPages);
+                const int per = (pages + n_parts - 1) / n_parts;
+                int group_id = -1, part_base = 0;
+                if (n_parts > 1) {
+                    group_id = P.n_groups++;
+                    part_base = P.n_parts;
+                    P.n_parts += n_parts;
+                    if (kvh == 0) ++P.n_split_spans;
+                }
+                for (int part = 0; part < n_parts; ++part) {
+                    WorkItem w{};
+                    w.span = si;
+                    w.kvh = kvh;
+                    w.type = kWorkDecode;
+                    w.t0 = 0;
+                    w.nt = 1;
+                    w.n_parts = static_cast<int16_t>(n_parts);
+                    w.part_idx = static_cast<int16_t>(part);
+                    w.kv_begin = part * per * s.chunk_size;
+                    w.kv_end = std::min(sp.context_len, (part + 1) * per * s.chunk_size);
+                    w.group = group_id;
+                    w.part_base = part_base;
+                    tc_list.push_back({static_cast<double>(w.kv_end - w.kv_begin), w});
+                    ++P.n_decode;
+                }
+            }
+        }
+    }
+    // Heavy items first so the persistent CTAs finish together (LPT order).
+    std::stable_sort(tc_list.begin(), tc_list.end(),
+                     [](const auto& a, const auto& b) { return a.first > b.first; });
+    P.tc_items.reserve(tc_list.size());
+    for (auto& e : tc_list) P.tc_items.push_back(e.second);
+}
+
+} // namespace
+
+extern "C" {
+
+pb_status pb_attn_plan_create(const pb_attn_shape* shape, int32_t n_spans,
+                              const int64_t* query_start, const int64_t* query_len,
+                              const int64_t* context_len, const int64_t* causal_offset,
+                              const int32_t* block_tables, const int64_t* block_table_offsets,
+                              int64_t total_tokens, int32_t flags, pb_attn_plan** out) {
+    return guarded([&] {
+        if (!shape || !out) fail(PB_ERR_ERROR, "null argument");
+        *out = nullptr;
+        validate(*shape, n_spans, query_start, query_len, context_len, causal_offset,
+                 block_tables, block_table_offsets, total_tokens, nullptr);
+        if (flags & PB_PLAN_SINGLE_TOKEN)
+            for (int32_t i = 0; i < n_spans; ++i)
+                require(query_len[i] == 1, "single-token path requires query_len == 1 spans");
+        if (shape->head_size > 256) fail(PB_ERR_UNSUPPORTED, "head_size > 256");
+        auto P = std::make_unique<pb_attn_plan>();
+        P->shape = *shape;
+        P->flags = flags;
+        P->group = shape->n_head / shape->n_kv_head;
+        P->total_tokens = total_tokens;
+        const int64_t n_bt = n_spans > 0 ? block_table_offsets[n_spans] - block_table_offsets[0] : 0;
+        P->bt.assign(block_tables + (n_spans > 0 ? block_table_offsets[0] : 0),
+                     block_tables + (n_spans > 0 ? block_table_offsets[0] : 0) + n_bt);
+        const int eb = dtype_bytes(shape->dtype);
+        const double d = shape->head_size;
+        for (int32_t i = 0; i < n_spans; ++i) {
+            SpanDev sp{};
+            sp.query_start = static_cast<int32_t>(query_start[i]);
+            sp.query_len = static_cast<int32_t>(query_len[i]);
+            sp.causal_offset = static_cast<int32_t>(causal_offset[i]);
+            sp.context_len = static_cast<int32_t>(context_len[i]);
+            sp.bt_off = block_table_offsets[i] - block_table_offsets[0];
+            sp.n_pages = static_cast<int32_t>(block_table_offsets[i + 1] - block_table_offsets[i]);
+            P->spans.push_back(sp);
+            // unmasked score pairs only; K+V once per kv head; Q, O, table.
+            const double q = static_cast<double>(query_len[i]);
+            const double allowed_sum = q * static_cast<double>(causal_offset[i]) + q * (q + 1) / 2;
+            P->flops += 4.0 * shape->n_head * d * allowed_sum;
+            if (query_len[i] > 0)
+                P->bytes += 2.0 * context_len[i] * shape->n_kv_head * d * eb +
+                            2.0 * q * shape->n_head * d * eb + 4.0 * sp.n_pages;
+        }
+        build_work(*P);
+        *out = P.release();
+    });
+}
+
+pb_status pb_attn_plan_upload(pb_attn_plan* P, void* stream) {
+    return guarded([&] {
+        if (!P) fail(PB_ERR_ERROR, "null plan");
+        const size_t b_spans = sizeof(SpanDev) * P->spans.size();
+        P->off_bt = align_up(b_spans, 256);
+        P->off_simt = align_up(P->off_bt + sizeof(int32_t) * P->bt.size(), 256);
+        P->off_tc = align_up(P->off_simt + sizeof(WorkItem) * P->simt_items.size(), 256);
+        const size_t total = std::max<size_t>(256, P->off_tc + sizeof(WorkItem) * P->tc_items.size());
+        if (P->d_bytes < total) {
+            if (P->d_buf) cudaFree(P->d_buf);
+            P->d_buf = nullptr;
+            cuda_check(cudaMalloc(&P->d_buf, total), "cudaMalloc(plan descriptors)");
+            P->d_bytes = total;
+        }
+        // One pinned staging copy so the H2D is a single async transfer.
+        std::vector<uint8_t> host(total, 0);
+        if (b_spans) std::memcpy(host.data(), P->spans.data(), b_spans);
+        if (!P->bt.empty()) std::memcpy(host.data() + P->off_bt, P->bt.data(), sizeof(int32_t) * P->bt.size());
+        if (!P->simt_items.empty())
+            std::memcpy(host.data() + P->off_simt, P->simt_items.data(), sizeof(WorkItem) * P->simt_items.size());
+        if (!P->tc_items.empty())
+            std::memcpy(host.data() + P->off_tc, P->tc_items.data(), sizeof(WorkItem) * P->tc_items.size());
+        cuda_check(cudaMemcpyAsync(P->d_buf, host.data(), total, cudaMemcpyHostToDevice, as_stream(stream)),
+                   "plan upload");
+        cuda_check(cudaStreamSynchronize(as_stream(stream)), "plan upload sync");
+        P->uploaded = true;
+    });
+}
+
+size_t pb_attn_plan_workspace_bytes(const pb_attn_plan* P) {
+    if (!P) return 0;
+    const size_t g = static_cast<size_t>(P->group);
+    size_t b = 256; // work counter + padding
+    b += align_up(sizeof(int32_t) * static_cast<size_t>(P->n_groups), 256);
+    b += align_up(sizeof(float) * 2 * g * static_cast<size_t>(P->n_parts), 256);
+    b += align_up(sizeof(float) * g * P->shape.head_size * static_cast<size_t>(P->n_parts), 256);
+    return b;
+}
+
+void pb_attn_plan_stats(const pb_attn_plan* P, double* o) {
+    if (!P || !o) return;
+    o[0] = P->n_prefill;
+    o[1] = P->n_decode;
+    o[2] = P->n_split_spans;
+    o[3] = P->flops;
+    o[4] = P->bytes;
+    o[5] = static_cast<double>(P->total_tokens);
+    o[6] = static_cast<double>(P->simt_items.size());
+    double rows = 0;
+    for (const auto& w : P->simt_items) rows += static_cast<double>(w.nt) * P->group;
+    for (const auto& w : P->tc_items)
+        if (w.type == kWorkPrefill || w.part_idx == 0) rows += static_cast<double>(w.nt) * P->group;
+    o[7] = rows;
+}
+
+static AttnParams make_params(pb_attn_plan* P, const void* q, const void* k, const void* v,
+                              void* out, void* ws) {
+    AttnParams p{};
+    p.n_head = P->shape.n_head;
+    p.n_kv_head = P->shape.n_kv_head;
+    p.head_size = P->shape.head_size;
+    p.chunk = P->shape.chunk_size;
+    p.n_slots = P->shape.n_slots;
+    p.group = P->group;
+    p.scale = static_cast<float>(P->shape.scale);
+    p.scale_log2 = static_cast<float>(1.4426950408889634 / P->shape.scale);
+    p.n_groups = P->n_groups;
+    auto* base = static_cast<uint8_t*>(P->d_buf);
+    p.spans = reinterpret_cast<const SpanDev*>(base);
+    p.block_tables = reinterpret_cast<const int32_t*>(base + P->off_bt);
+    p.q = q;
+    p.k_pages = k;
+    p.v_pages = v;
+    p.out = out;
+    auto* w = static_cast<uint8_t*>(ws);
+    if (w) {
+        const size_t g = static_cast<size_t>(P->group);
+        p.work_counter = reinterpret_cast<int32_t*>(w);
+        size_t off = 256;
+        p.counters = reinterpret_cast<int32_t*>(w + off);
+        off += align_up(sizeof(int32_t) * static_cast<size_t>(P->n_groups), 256);
+        p.part_ml = reinterpret_cast<float*>(w + off);
+        off += align_up(sizeof(float) * 2 * g * static_cast<size_t>(P->n_parts), 256);
+        p.part_o = reinterpret_cast<float*>(w + off);
+    }
+    return p;
+}
+
+pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const void* v_pages,
+                      void* out, void* workspace, void* stream) {
+    return guarded([&] {
+        if (!P) fail(PB_ERR_ERROR, "null plan");
+        if (!P->uploaded) fail(PB_ERR_ERROR, "plan not uploaded (call pb_attn_plan_upload)");
+        if (P->total_tokens == 0) return;
+        if (!q || !k_pages || !v_pages || !out) fail(PB_ERR_ERROR, "null device pointer");
+        if (!P->tc_items.empty() && !workspace) fail(PB_ERR_ERROR, "workspace required");
+        cudaStream_t st = as_stream(stream);
+        AttnParams p = make_params(P, q, k_pages, v_pages, out, workspace);
+        if (workspace && workspace != P->last_workspace) {
+            // counters are self-resetting; zero them once per workspace buffer
+            cuda_check(cudaMemsetAsync(workspace, 0, 256 + align_up(sizeof(int32_t) * P->n_groups, 256), st),
+                       "workspace init");
+            P->last_workspace = workspace;
+        }
+        if (!P->simt_items.empty()) {
+            AttnParams ps = p;
+            ps.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_simt);
+            ps.n_items = static_cast<int32_t>(P->simt_items.size());
+            launch_attn_simt(ps, P->shape.dtype, ps.n_items, st);
+        }
+        if (!P->tc_items.empty()) {
+            AttnParams pt = p;
+            pt.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_tc);
+            pt.n_items = static_cast<int32_t>(P->tc_items.size());
+            launch_attn_sm100(pt, P->shape, P->sm100, P->total_tokens, st);
+        }
+    });
+}
+
+pb_status pb_attn_check_numerics(pb_attn_plan* P, const void* q, const void* k_pages,
+                                 int32_t* d_flag, void* stream) {
+    return guarded([&] {
+        if (!P || !P->uploaded) fail(PB_ERR_ERROR, "plan not uploaded");
+        AttnParams p = make_params(P, q, k_pages, nullptr, nullptr, nullptr);
+        p.n_items = static_cast<int32_t>(P->spans.size());
+        launch_check_numerics(p, P->shape.dtype, P->total_tokens * P->shape.n_head * P->shape.head_size,
+                              d_flag, as_stream(stream));
+    });
+}
+
+void pb_attn_plan_destroy(pb_attn_plan* P) {
+    if (!P) return;
+    if (P->d_buf) cudaFree(P->d_buf);
+    sm100_cache_release(P->sm100);
+    delete P;
+}
+
+} // extern "C"
+
+// Host-side helpers for the one-shot API (api_host.cu).
+namespace pb {
+void plan_validate_with_q(const pb_attn_shape& s, int32_t n_spans, const int64_t* qs,
+                          const int64_t* ql, const int64_t* cl, const int64_t* co,
+                          const int32_t* bt, const int64_t* bt_off, int64_t total_tokens,
+                          const float* q_host) {
+    validate(s, n_spans, qs, ql, cl, co, bt, bt_off, total_tokens, q_host);
+}
+} // namespace pb

@@ -1,0 +1,30 @@
+// sm_100a tile path of the fused ragged paged attention (see sm100_attn.cu).
+#pragma once
+
+#include "attn_internal.hpp"
+#include "pensieve_b200.h"
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+namespace pb {
+
+// Host-side cache of the TMA tensor maps of the last launch (re-encoded only when the
+// q / page pointers or shapes change).
+struct Sm100Cache {
+    const void* q = nullptr;
+    const void* k = nullptr;
+    const void* v = nullptr;
+    int64_t total_tokens = -1;
+    alignas(64) unsigned char maps[3][128];
+    bool valid = false;
+};
+
+bool sm100_supports(int head_size, int chunk, int group);
+int sm100_tile_tokens(int group);
+void launch_attn_sm100(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache,
+                       int64_t total_tokens, cudaStream_t stream);
+void sm100_cache_release(Sm100Cache& cache);
+
+} // namespace pb

@@ -1,0 +1,55 @@
+"""Device-side harness for the GPU parity tests: builds a workload's pools and queries in
+HBM through the product's own fill kernel, runs a plan, and builds compact CPU-oracle inputs
+for sampled spans (the oracle only needs the pages those spans touch)."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+from paper_2312_05516_b200 import abi
+from paper_2312_05516_b200.abi import PB_BF16, PB_F32, AttentionPlan, Batch
+from paper_2312_05516_b200.workloads import Workload, round_bf16
+
+TORCH_DT = {PB_F32: torch.float32, PB_BF16: torch.bfloat16}
+
+
+def device_inputs(w: Workload, layer: int = 0, dev: str = "cuda:0"):
+    dt = TORCH_DT[w.dtype]
+    k = torch.empty(max(1, w.pool_elems), dtype=dt, device=dev)
+    v = torch.empty_like(k)
+    q = torch.empty(max(1, w.q_elems), dtype=dt, device=dev)
+    abi.fill_unit(k.data_ptr(), w.dtype, w.pool_elems, w.seed, w.k_first_draw(layer))
+    abi.fill_unit(v.data_ptr(), w.dtype, w.pool_elems, w.seed, w.v_first_draw(layer))
+    abi.fill_unit(q.data_ptr(), w.dtype, w.q_elems, w.seed, w.q_first_draw())
+    return q, k, v
+
+
+def run_plan(w: Workload, q, k, v, flags: int = 0, batch: Batch = None, shape=None):
+    shape = shape or w.shape()
+    batch = batch or w.batch()
+    plan = AttentionPlan(shape, batch, flags)
+    stream = torch.cuda.current_stream().cuda_stream
+    plan.upload(stream)
+    out = torch.zeros(max(1, batch.total_tokens * shape.n_head * shape.head_size), dtype=q.dtype,
+                      device=q.device)
+    ws = torch.zeros(max(1, plan.workspace_bytes()), dtype=torch.uint8, device=q.device)
+    plan.run(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), ws.data_ptr(), stream)
+    torch.cuda.synchronize()
+    return out.float().cpu().numpy()[: batch.total_tokens * shape.n_head * shape.head_size], plan
+
+
+def sampled_oracle_inputs(w: Workload, span_ids, layer: int = 0):
+    return w.compact_host_inputs(span_ids, layer)
+
+
+def gather_out_rows(out: np.ndarray, w: Workload, span_ids) -> np.ndarray:
+    rows = out.reshape(w.total_tokens, w.n_head * w.head_size)
+    tok = w.span_token_offsets()
+    return np.concatenate([rows[tok[i]:tok[i + 1]] for i in span_ids]).reshape(-1)
+
+
+def bf16_close(got: np.ndarray, ref: np.ndarray, atol: float = 2e-2, rtol: float = 1e-2):
+    """North-star bf16 parity: |got - ref| <= 2e-2 + 1e-2 * |ref| elementwise."""
+    err = np.abs(got.astype(np.float64) - ref.astype(np.float64))
+    bound = atol + rtol * np.abs(ref.astype(np.float64))
+    return bool(np.all(err <= bound)), float(err.max(initial=0.0))
