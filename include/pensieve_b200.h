@@ -170,6 +170,82 @@ pb_status pb_kv_append(const pb_attn_shape* shape, int32_t n_spans, const int64_
 pb_status pb_fill_splitmix_unit(void* dst, int32_t dtype, int64_t n, uint64_t seed,
                                 uint64_t first_draw, void* stream);
 
+/* ===================================================================== KV page bookkeeping
+ * Two-tier slot allocator + per-conversation chunk index with the exact slot semantics of
+ * kvsim::PagedKvCache (include/kvsim/paged_kv_cache.hpp:52-153, src/paged_kv_cache.cpp):
+ * lowest slot ids first, device slots vacated by swap-out reused LIFO before free ones,
+ * fill-partial-first appends, validate-before-mutate.  Block tables and slot lists are
+ * bit-identical to the reference.  In addition every tier move reports its
+ * (chunk, source slot, destination slot) triple, which the copy engine needs and the
+ * reference discards.  Host-only; single writer. */
+typedef struct pb_kv_cache pb_kv_cache;
+
+typedef struct pb_slot_move {
+    int64_t chunk;
+    int32_t src_slot; /* slot in the tier the chunk left (-1: rematerialised from nothing) */
+    int32_t dst_slot; /* slot in the tier it entered (-1: dropped) */
+} pb_slot_move;
+
+typedef struct pb_chunk_record { /* ChunkRecord, include/kvsim/chunk.hpp:23-33 */
+    int64_t chunk_id, conv_id, start_offset, n_tokens;
+    int32_t location; /* 0 device, 1 host, 2 dropped (ChunkLocationKind) */
+    int32_t slot;
+    double last_active;
+} pb_chunk_record;
+
+typedef struct pb_layout_segment { /* LayoutSegment, paged_kv_cache.hpp:20-27 */
+    int32_t kind;     /* 0 resident (device), 1 swap-in (host), 2 recompute (dropped) */
+    int32_t n_chunks;
+    int64_t token_begin, token_end;
+    int64_t first_chunk;
+} pb_layout_segment;
+
+/* PagedKvCache(chunk_size, device_slots, host_slots)        paged_kv_cache.cpp:12-26 */
+pb_status pb_cache_create(int32_t chunk_size, int32_t device_slots, int32_t host_slots,
+                          pb_kv_cache** out);
+void pb_cache_destroy(pb_kv_cache* cache);
+/* allocate(conv, n_tokens, now) -> created chunk ids         paged_kv_cache.cpp:53-96 */
+pb_status pb_cache_allocate(pb_kv_cache* cache, int64_t conv, int64_t n_tokens, double now,
+                            int64_t* created, int64_t cap, int64_t* n_created);
+/* apply_evictions(victims, Host|Dropped); moves[i] for ids[i]  paged_kv_cache.cpp:129-172 */
+pb_status pb_cache_apply_evictions(pb_kv_cache* cache, const int64_t* ids, int64_t n,
+                                   int32_t to_host, pb_slot_move* moves);
+/* restore(chunks): host slot -> device slot                   paged_kv_cache.cpp:174-197 */
+pb_status pb_cache_restore(pb_kv_cache* cache, const int64_t* ids, int64_t n, pb_slot_move* moves);
+/* rematerialize(chunks): dropped -> device slot               paged_kv_cache.cpp:199-220 */
+pb_status pb_cache_rematerialize(pb_kv_cache* cache, const int64_t* ids, int64_t n,
+                                 pb_slot_move* moves);
+/* release_conversation(conv)                                  paged_kv_cache.cpp:224-246 */
+pb_status pb_cache_release_conversation(pb_kv_cache* cache, int64_t conv);
+/* touch / retain_on_finish(conv, now)                         paged_kv_cache.cpp:222-254 */
+pb_status pb_cache_touch(pb_kv_cache* cache, int64_t conv, double now);
+/* block_table(conv, context_tokens)                           paged_kv_cache.cpp:284-304 */
+pb_status pb_cache_block_table(const pb_kv_cache* cache, int64_t conv, int64_t context_tokens,
+                               int32_t* out, int64_t cap, int64_t* n);
+/* layout(conv)                                                paged_kv_cache.cpp:98-127 */
+pb_status pb_cache_layout(const pb_kv_cache* cache, int64_t conv, pb_layout_segment* segs,
+                          int64_t cap, int64_t* n, int64_t* total_tokens);
+/* conversation_chunks(conv) with their records                paged_kv_cache.hpp:104 */
+pb_status pb_cache_conversation_chunks(const pb_kv_cache* cache, int64_t conv,
+                                       pb_chunk_record* out, int64_t cap, int64_t* n);
+/* chunk(id)                                                   paged_kv_cache.hpp:103 */
+pb_status pb_cache_chunk(const pb_kv_cache* cache, int64_t id, pb_chunk_record* out);
+/* collect_chunks(kind, exclude) in (conv, offset) order       paged_kv_cache.cpp:270-282 */
+pb_status pb_cache_collect_chunks(const pb_kv_cache* cache, int32_t location,
+                                  const int64_t* exclude_convs, int64_t n_exclude, int64_t* ids,
+                                  int64_t cap, int64_t* n);
+/* counts[8]: device capacity, free, reclaimable, allocated; host capacity, free, allocated;
+ * chunk size */
+void pb_cache_counts(const pb_kv_cache* cache, int64_t* counts8);
+int32_t pb_cache_has_conversation(const pb_kv_cache* cache, int64_t conv);
+int64_t pb_cache_total_tokens(const pb_kv_cache* cache, int64_t conv);
+/* append_chunks_needed(conv, add)                             paged_kv_cache.cpp:306-312 */
+int32_t pb_cache_append_chunks_needed(const pb_kv_cache* cache, int64_t conv, int64_t add);
+/* verify(): PB_ERR_ERROR on any invariant violation           paged_kv_cache.cpp:341-396 */
+pb_status pb_cache_verify(const pb_kv_cache* cache);
+/* dump() text; returns its length, writes at most cap-1 chars  paged_kv_cache.cpp:314-339 */
+int64_t pb_cache_dump(const pb_kv_cache* cache, char* buf, int64_t cap);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

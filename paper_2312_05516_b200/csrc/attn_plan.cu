@@ -32,7 +32,9 @@ struct pb_attn_plan {
     std::vector<SpanDev> spans;
     std::vector<int32_t> bt;
     std::vector<WorkItem> simt_items;
-    std::vector<WorkItem> tc_items; // prefill tiles + decode units for the sm_100a kernel
+    std::vector<WorkItem> tc_items;     // prefill tiles for the sm_100a tcgen05 kernel
+    std::vector<WorkItem> decode_items; // single-token split-KV units
+    bool decode_kernel = false;         // decode units built (else decode spans go SIMT)
     int32_t n_groups = 0;
     int32_t n_parts = 0;
     int32_t n_prefill = 0, n_decode = 0, n_split_spans = 0;
@@ -40,7 +42,7 @@ struct pb_attn_plan {
     // device copies: [spans | block tables | simt items | tc items]
     void* d_buf = nullptr;
     size_t d_bytes = 0;
-    size_t off_bt = 0, off_simt = 0, off_tc = 0;
+    size_t off_bt = 0, off_simt = 0, off_tc = 0, off_dec = 0;
     bool uploaded = false;
     void* last_workspace = nullptr;
     Sm100Cache sm100;
@@ -102,7 +104,8 @@ void build_work(pb_attn_plan& P) {
     // SIMT tiles: blocks of tokens, ~16 rows per warp-pass
     const int simt_tokens = std::max(1, 32 / g);
     const int tc_tokens = tc ? sm100_tile_tokens(g) : 0;
-    std::vector<std::pair<double, WorkItem>> tc_list;
+    P.decode_kernel = tc && decode_supports(s.head_size, s.chunk_size, g);
+    std::vector<std::pair<double, WorkItem>> tc_list, dec_list;
     for (int32_t si = 0; si < static_cast<int32_t>(P.spans.size()); ++si) {
         const SpanDev& sp = P.spans[si];
         if (sp.query_len == 0) continue;
@@ -131,6 +134,15 @@ void build_work(pb_attn_plan& P) {
                     tc_list.push_back({kv * 4.0, w}); // tensor tile ~ 4x a decode page pass
                     ++P.n_prefill;
                 }
+            } else if (!P.decode_kernel) {
+                WorkItem w{};
+                w.span = si;
+                w.kvh = kvh;
+                w.type = kWorkSimt;
+                w.t0 = 0;
+                w.nt = 1;
+                w.group = -1;
+                P.simt_items.push_back(w);
             } else {
                 const int pages = sp.n_pages;
                 const int n_parts = (P.flags & PB_PLAN_NO_SPLIT)
@@ -157,7 +169,7 @@ void build_work(pb_attn_plan& P) {
                     w.kv_end = std::min(sp.context_len, (part + 1) * per * s.chunk_size);
                     w.group = group_id;
                     w.part_base = part_base;
-                    tc_list.push_back({static_cast<double>(w.kv_end - w.kv_begin), w});
+                    dec_list.push_back({static_cast<double>(w.kv_end - w.kv_begin), w});
                     ++P.n_decode;
                 }
             }
@@ -166,8 +178,11 @@ void build_work(pb_attn_plan& P) {
     // Heavy items first so the persistent CTAs finish together (LPT order).
     std::stable_sort(tc_list.begin(), tc_list.end(),
                      [](const auto& a, const auto& b) { return a.first > b.first; });
+    std::stable_sort(dec_list.begin(), dec_list.end(),
+                     [](const auto& a, const auto& b) { return a.first > b.first; });
     P.tc_items.reserve(tc_list.size());
     for (auto& e : tc_list) P.tc_items.push_back(e.second);
+    for (auto& e : dec_list) P.decode_items.push_back(e.second);
 }
 
 } // namespace
@@ -227,7 +242,8 @@ pb_status pb_attn_plan_upload(pb_attn_plan* P, void* stream) {
         P->off_bt = align_up(b_spans, 256);
         P->off_simt = align_up(P->off_bt + sizeof(int32_t) * P->bt.size(), 256);
         P->off_tc = align_up(P->off_simt + sizeof(WorkItem) * P->simt_items.size(), 256);
-        const size_t total = std::max<size_t>(256, P->off_tc + sizeof(WorkItem) * P->tc_items.size());
+        P->off_dec = align_up(P->off_tc + sizeof(WorkItem) * P->tc_items.size(), 256);
+        const size_t total = std::max<size_t>(256, P->off_dec + sizeof(WorkItem) * P->decode_items.size());
         if (P->d_bytes < total) {
             if (P->d_buf) cudaFree(P->d_buf);
             P->d_buf = nullptr;
@@ -242,6 +258,8 @@ pb_status pb_attn_plan_upload(pb_attn_plan* P, void* stream) {
             std::memcpy(host.data() + P->off_simt, P->simt_items.data(), sizeof(WorkItem) * P->simt_items.size());
         if (!P->tc_items.empty())
             std::memcpy(host.data() + P->off_tc, P->tc_items.data(), sizeof(WorkItem) * P->tc_items.size());
+        if (!P->decode_items.empty())
+            std::memcpy(host.data() + P->off_dec, P->decode_items.data(), sizeof(WorkItem) * P->decode_items.size());
         cuda_check(cudaMemcpyAsync(P->d_buf, host.data(), total, cudaMemcpyHostToDevice, as_stream(stream)),
                    "plan upload");
         cuda_check(cudaStreamSynchronize(as_stream(stream)), "plan upload sync");
@@ -270,8 +288,9 @@ void pb_attn_plan_stats(const pb_attn_plan* P, double* o) {
     o[6] = static_cast<double>(P->simt_items.size());
     double rows = 0;
     for (const auto& w : P->simt_items) rows += static_cast<double>(w.nt) * P->group;
-    for (const auto& w : P->tc_items)
-        if (w.type == kWorkPrefill || w.part_idx == 0) rows += static_cast<double>(w.nt) * P->group;
+    for (const auto& w : P->tc_items) rows += static_cast<double>(w.nt) * P->group;
+    for (const auto& w : P->decode_items)
+        if (w.part_idx == 0) rows += static_cast<double>(w.nt) * P->group;
     o[7] = rows;
 }
 
@@ -315,7 +334,8 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
         if (!P->uploaded) fail(PB_ERR_ERROR, "plan not uploaded (call pb_attn_plan_upload)");
         if (P->total_tokens == 0) return;
         if (!q || !k_pages || !v_pages || !out) fail(PB_ERR_ERROR, "null device pointer");
-        if (!P->tc_items.empty() && !workspace) fail(PB_ERR_ERROR, "workspace required");
+        if ((!P->tc_items.empty() || !P->decode_items.empty()) && !workspace)
+            fail(PB_ERR_ERROR, "workspace required");
         cudaStream_t st = as_stream(stream);
         AttnParams p = make_params(P, q, k_pages, v_pages, out, workspace);
         if (workspace && workspace != P->last_workspace) {
@@ -335,6 +355,12 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
             pt.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_tc);
             pt.n_items = static_cast<int32_t>(P->tc_items.size());
             launch_attn_sm100(pt, P->shape, P->sm100, P->total_tokens, st);
+        }
+        if (!P->decode_items.empty()) {
+            AttnParams pd = p;
+            pd.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_dec);
+            pd.n_items = static_cast<int32_t>(P->decode_items.size());
+            launch_attn_decode(pd, P->shape, P->sm100, P->total_tokens, st);
         }
     });
 }

@@ -1,11 +1,407 @@
-// placeholder: replaced by the tcgen05 tile kernel
-#include "sm100_attn.hpp"
+// sm_100a tile path of the fused ragged paged attention: multi-token spans (prefill, prompt
+// and dropped-prefix recompute spans) on the 5th-generation tensor cores.
+//
+// Semantics: paged_multi_token_attention, /root/reference/proj/src/attention.cpp:73-132
+// (token i of a span sees [0, causal_offset+i], head h reads kv head h/group, softmax with
+// max subtraction).  B200 design:
+//   * one work item = (span, kv head, block of 128/group query tokens); the GQA group is packed
+//     into the M dimension, so M = 128 rows = tokens x heads-of-the-group (PAPER.md:708-717
+//     fuses QK^T, mask, softmax, PV in one kernel; here on tcgen05 with TMEM accumulators);
+//   * persistent CTAs, 6 warps: warp 0 = TMA producer, warp 1 = MMA issuer (single elected
+//     thread, tcgen05.mma.cta_group::1.kind::f16, accumulators in TMEM), warps 2-5 =
+//     softmax / correction / epilogue, one TMEM lane (= one query row) per thread;
+//   * KV pages are gathered straight from the paged pools by TMA: a 128-row KV tile is
+//     128/page_tokens box loads {64 dims, 1 kv head, page_tokens rows} at row coordinate
+//     block_table[p] * page_tokens (SWIZZLE_128B); pages past the span's table are fetched
+//     out of bounds, which TMA zero-fills;
+//   * S = Q K^T double-buffered in TMEM (S_{j+1} is issued before P_j V_j), P written to
+//     shared memory in the UMMA K-major SW128 layout, O accumulated in TMEM, rescaled lazily
+//     (only when the running max grows by more than 2^8).
+#include "attn_internal.hpp"
 #include "pb_common.hpp"
+#include "sm100_attn.hpp"
+#include "sm100_ptx.cuh"
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_bf16.h>
+#include <math_constants.h>
+
+#include <algorithm>
+#include <cstring>
+
 namespace pb {
-bool sm100_supports(int, int, int) { return false; }
-int sm100_tile_tokens(int group) { return 128 / group; }
-void launch_attn_sm100(const AttnParams&, const pb_attn_shape&, Sm100Cache&, int64_t, cudaStream_t) {
-    fail(PB_ERR_UNSUPPORTED, "sm100 path not built");
+
+namespace {
+
+using namespace pb::sm100;
+
+constexpr int kThreads = 192;
+constexpr int kTileRows = 128;       // M rows per work item and kv rows per tile
+constexpr uint32_t kTmemCols = 512;  // S0 [0,128) S1 [128,256) O [256, 256+D)
+constexpr uint32_t kColO = 256;
+constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max grows by > 2^8
+
+template <int D>
+struct __align__(1024) Smem {
+    uint8_t q[kTileRows * D * 2];     // [D/64][128 rows][128 B] K-major SW128
+    uint8_t k[2][kTileRows * D * 2];  // 2-stage ring, same layout
+    uint8_t v[2][kTileRows * D * 2];  // 2-stage ring; read as MN-major SW128 B operand
+    uint8_t p[kTileRows * kTileRows * 2]; // [2 kv halves][128 rows][128 B]
+    uint64_t q_full, q_empty;
+    uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
+    uint64_t s_full[2], s_empty[2];
+    uint64_t p_full, o_ready, o_empty;
+    uint32_t tmem_base;
+};
+
+__device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+    attn_prefill_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                              const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
+    constexpr int KH = D / 64;                  // 64-dim halves (one 128 B swizzle row each)
+    constexpr uint32_t kHalfBytes = kTileRows * 128;
+    constexpr uint32_t kTileBytes = kTileRows * D * 2;
+    extern __shared__ uint8_t smem_raw[];
+    Smem<D>& s = *reinterpret_cast<Smem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    const int g = p.group;
+    const int tpt = kTileRows / g;         // query tokens per tile
+    const int chunk = p.chunk;
+    const int ppt = kTileRows / chunk;     // pages per kv tile
+
+    if (threadIdx.x == 0) {
+        mbar_init(&s.q_full, 1);
+        mbar_init(&s.q_empty, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&s.k_full[i], 1);
+            mbar_init(&s.k_empty[i], 1);
+            mbar_init(&s.v_full[i], 1);
+            mbar_init(&s.v_empty[i], 1);
+            mbar_init(&s.s_full[i], 1);
+            mbar_init(&s.s_empty[i], 128);
+        }
+        mbar_init(&s.p_full, 128);
+        mbar_init(&s.o_ready, 1);
+        mbar_init(&s.o_empty, 128);
+        mbar_fence_init();
+        tma_prefetch(&tm_q);
+        tma_prefetch(&tm_k);
+        tma_prefetch(&tm_v);
+    }
+    if (warp == 1) tmem_alloc<kTmemCols>(&s.tmem_base);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = s.tmem_base;
+
+    if (warp == 0) {
+        // ============================ TMA producer ============================
+        if (elect_one()) {
+            int it = 0, kst = 0, vst = 0;
+            uint32_t kph = 0, vph = 0;
+            const uint32_t q_bytes = KH * 128u * static_cast<uint32_t>(g * tpt);
+            const int oob_row = p.n_slots * chunk;
+            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+                const WorkItem w = p.items[item];
+                const SpanDev sp = p.spans[w.span];
+                const int32_t* table = p.block_tables + sp.bt_off;
+                const int n_tiles = ceil_div(sp.causal_offset + w.t0 + w.nt, kTileRows);
+                if (it > 0) mbar_wait(&s.q_empty, (it - 1) & 1);
+                mbar_arrive_expect_tx(&s.q_full, q_bytes);
+                for (int h = 0; h < KH; ++h)
+                    tma_load_3d(s.q + h * kHalfBytes, &tm_q, &s.q_full, h * 64, w.kvh * g, sp.query_start + w.t0);
+                for (int j = 0; j < n_tiles; ++j) {
+                    for (int which = 0; which < 2; ++which) {
+                        uint64_t* full = which ? &s.v_full[vst] : &s.k_full[kst];
+                        uint64_t* empty = which ? &s.v_empty[vst] : &s.k_empty[kst];
+                        uint8_t* dst = which ? s.v[vst] : s.k[kst];
+                        const CUtensorMap* tm = which ? &tm_v : &tm_k;
+                        mbar_wait(empty, (which ? vph : kph) ^ 1);
+                        mbar_arrive_expect_tx(full, kTileBytes);
+                        for (int pg = 0; pg < ppt; ++pg) {
+                            const int page = j * ppt + pg;
+                            const int row = page < sp.n_pages ? table[page] * chunk : oob_row;
+                            for (int h = 0; h < KH; ++h)
+                                tma_load_3d(dst + h * kHalfBytes + pg * chunk * 128, tm, full, h * 64, w.kvh, row);
+                        }
+                        if (which) {
+                            if (++vst == 2) { vst = 0; vph ^= 1; }
+                        } else {
+                            if (++kst == 2) { kst = 0; kph ^= 1; }
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ============================ MMA issuer =============================
+        if (elect_one()) {
+            constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
+            constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
+            const uint32_t q_addr = smem_u32(s.q);
+            const uint32_t p_addr = smem_u32(s.p);
+            int it = 0, kst = 0, vst = 0;
+            uint32_t kph = 0, vph = 0, n_s = 0, n_p = 0;
+            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+                const WorkItem w = p.items[item];
+                const SpanDev sp = p.spans[w.span];
+                const int n_tiles = ceil_div(sp.causal_offset + w.t0 + w.nt, kTileRows);
+                mbar_wait(&s.q_full, it & 1);
+                tc_fence_after();
+                auto issue_s = [&]() {
+                    const uint32_t sb = n_s & 1;
+                    mbar_wait(&s.k_full[kst], kph);
+                    mbar_wait(&s.s_empty[sb], ((n_s >> 1) & 1) ^ 1);
+                    tc_fence_after();
+                    const uint32_t k_addr = smem_u32(s.k[kst]);
+#pragma unroll
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
+                        umma_bf16_ss(tmem + sb * 128, umma_desc_sw128(q_addr + off, 16, 1024),
+                                     umma_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0);
+                    }
+                    umma_commit(&s.k_empty[kst]);
+                    umma_commit(&s.s_full[sb]);
+                    if (++kst == 2) { kst = 0; kph ^= 1; }
+                    ++n_s;
+                };
+                issue_s();
+                if (n_tiles > 1) issue_s();
+                for (int j = 0; j < n_tiles; ++j) {
+                    mbar_wait(&s.p_full, n_p & 1);
+                    ++n_p;
+                    if (j == 0) mbar_wait(&s.o_empty, (it & 1) ^ 1);
+                    mbar_wait(&s.v_full[vst], vph);
+                    tc_fence_after();
+                    const uint32_t v_addr = smem_u32(s.v[vst]);
+#pragma unroll
+                    for (int kk = 0; kk < kTileRows / 16; ++kk) {
+                        const uint32_t a_off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
+                        umma_bf16_ss(tmem + kColO, umma_desc_sw128(p_addr + a_off, 16, 1024),
+                                     umma_desc_sw128(v_addr + kk * 2048, kHalfBytes, 1024), idesc_o,
+                                     (j > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&s.v_empty[vst]);
+                    umma_commit(&s.o_ready);
+                    if (++vst == 2) { vst = 0; vph ^= 1; }
+                    if (j + 2 < n_tiles) issue_s();
+                }
+                umma_commit(&s.q_empty);
+            }
+        }
+    } else {
+        // ===================== softmax / correction / epilogue =====================
+        const int quad = warp & 3;                 // TMEM lane quadrant of this warp
+        const int row = quad * 32 + lane;          // query row of this thread
+        const uint32_t t_lane = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+        const float sl2 = p.scale_log2;
+        uint32_t n_s = 0, n_o = 0;
+        int it = 0;
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+        for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+            const WorkItem w = p.items[item];
+            const SpanDev sp = p.spans[w.span];
+            const int n_tiles = ceil_div(sp.causal_offset + w.t0 + w.nt, kTileRows);
+            const int t_local = row / g;
+            const bool valid = t_local < w.nt && row < g * tpt;
+            const int allowed = sp.causal_offset + w.t0 + (valid ? t_local : 0) + 1;
+            float m_run = -CUDART_INF_F, l_run = 0.f;
+            for (int j = 0; j < n_tiles; ++j) {
+                const uint32_t sb = n_s & 1;
+                mbar_wait(&s.s_full[sb], (n_s >> 1) & 1);
+                ++n_s;
+                tc_fence_after();
+                float x[128];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) tmem_ld32(t_lane + sb * 128 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
+                tmem_ld_wait();
+                tc_fence_before();
+                mbar_arrive(&s.s_empty[sb]);
+                // causal mask + running max (log2 domain)
+                const int kv0 = j * kTileRows;
+                float mt = -CUDART_INF_F;
+#pragma unroll
+                for (int c = 0; c < 128; ++c) {
+                    const float v = (kv0 + c < allowed) ? x[c] * sl2 : -CUDART_INF_F;
+                    x[c] = v;
+                    mt = fmaxf(mt, v);
+                }
+                const bool grow = mt > m_run + kRescaleThreshold;
+                const float m_new = grow ? mt : m_run;
+                const float corr = grow ? ex2(m_run - m_new) : 1.f;
+                float sum = 0.f;
+#pragma unroll
+                for (int c = 0; c < 128; ++c) {
+                    x[c] = ex2(x[c] - m_new);
+                    sum += x[c];
+                }
+                l_run = l_run * corr + sum;
+                m_run = m_new;
+                if (j > 0) {
+                    // P_{j-1} V_{j-1} must be done before O is rescaled and P is overwritten
+                    mbar_wait(&s.o_ready, n_o & 1);
+                    ++n_o;
+                    tc_fence_after();
+                    if (__any_sync(0xffffffffu, grow)) {
+#pragma unroll
+                        for (int c = 0; c < D / 32; ++c) {
+                            uint32_t o[32];
+                            tmem_ld32(t_lane + kColO + c * 32, o);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+                            tmem_st32(t_lane + kColO + c * 32, o);
+                        }
+                        tmem_st_wait();
+                    }
+                }
+                // P (bf16) -> shared memory, UMMA K-major SW128: [kv half][row][128 B]
+                uint8_t* prow = s.p + (row >> 3) * 1024 + (row & 7) * 128;
+#pragma unroll
+                for (int cc = 0; cc < 16; ++cc) {
+                    const int kb = cc >> 3, c8 = cc & 7;
+                    uint4 v;
+                    v.x = pack_bf16x2(x[cc * 8 + 0], x[cc * 8 + 1]);
+                    v.y = pack_bf16x2(x[cc * 8 + 2], x[cc * 8 + 3]);
+                    v.z = pack_bf16x2(x[cc * 8 + 4], x[cc * 8 + 5]);
+                    v.w = pack_bf16x2(x[cc * 8 + 6], x[cc * 8 + 7]);
+                    *reinterpret_cast<uint4*>(prow + kb * kHalfBytes + ((c8 ^ (row & 7)) << 4)) = v;
+                }
+                fence_proxy_async_smem();
+                tc_fence_before();
+                mbar_arrive(&s.p_full);
+            }
+            // epilogue: O / l -> bf16 -> global
+            mbar_wait(&s.o_ready, n_o & 1);
+            ++n_o;
+            tc_fence_after();
+            const float inv_l = 1.f / l_run;
+            const int h = w.kvh * g + (row % g);
+            __nv_bfloat16* orow =
+                out + (static_cast<size_t>(sp.query_start + w.t0 + t_local) * p.n_head + h) * D;
+#pragma unroll
+            for (int c = 0; c < D / 32; ++c) {
+                uint32_t o[32];
+                tmem_ld32(t_lane + kColO + c * 32, o);
+                tmem_ld_wait();
+                if (valid) {
+#pragma unroll
+                    for (int e = 0; e < 32; e += 8) {
+                        uint4 v;
+                        v.x = pack_bf16x2(__uint_as_float(o[e + 0]) * inv_l, __uint_as_float(o[e + 1]) * inv_l);
+                        v.y = pack_bf16x2(__uint_as_float(o[e + 2]) * inv_l, __uint_as_float(o[e + 3]) * inv_l);
+                        v.z = pack_bf16x2(__uint_as_float(o[e + 4]) * inv_l, __uint_as_float(o[e + 5]) * inv_l);
+                        v.w = pack_bf16x2(__uint_as_float(o[e + 6]) * inv_l, __uint_as_float(o[e + 7]) * inv_l);
+                        *reinterpret_cast<uint4*>(orow + c * 32 + e) = v;
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&s.o_empty);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 1) {
+        tc_fence_after();
+        tmem_dealloc<kTmemCols>(tmem);
+    }
 }
-void sm100_cache_release(Sm100Cache&) {}
+
+// ------------------------------------------------------------------ host side
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q{};
+        cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q),
+                   "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
+        if (!f || q != cudaDriverEntryPointSuccess) fail(PB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
+        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }
+    return fn;
 }
+
+void encode_3d(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64_t d2, uint64_t s1_bytes,
+               uint64_t s2_bytes, uint32_t b0, uint32_t b1, uint32_t b2) {
+    cuuint64_t dims[3] = {d0, d1, d2};
+    cuuint64_t strides[2] = {s1_bytes, s2_bytes};
+    cuuint32_t box[3] = {b0, b1, b2};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = encode_fn()(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(ptr), dims, strides, box,
+                             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(PB_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
+}
+
+int g_sms = 0;
+
+template <int D>
+void launch_prefill(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st) {
+    const size_t smem = sizeof(Smem<D>) + 1024;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cuda_check(cudaFuncSetAttribute(attn_prefill_sm100_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        static_cast<int>(smem)),
+                   "cudaFuncSetAttribute(prefill smem)");
+        attr_set = true;
+    }
+    if (g_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int grid = std::min(p.n_items, g_sms);
+    attn_prefill_sm100_kernel<D><<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], p);
+    cuda_check(cudaGetLastError(), "attn_prefill_sm100 launch");
+    count_launch();
+}
+
+} // namespace
+
+bool sm100_supports(int head_size, int chunk, int group) {
+    return (head_size == 64 || head_size == 128) && chunk >= 8 && chunk <= 128 && (128 % chunk) == 0 &&
+           group >= 1 && group <= 128;
+}
+
+int sm100_tile_tokens(int group) { return kTileRows / group; }
+
+void sm100_prepare_maps(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens) {
+    const int D = shape.head_size;
+    const int g = shape.n_head / shape.n_kv_head;
+    if (!cache.valid || cache.q != p.q || cache.k != p.k_pages || cache.v != p.v_pages ||
+        cache.total_tokens != total_tokens) {
+        auto* m = reinterpret_cast<CUtensorMap*>(cache.maps);
+        encode_3d(&m[0], p.q, D, shape.n_head, std::max<int64_t>(total_tokens, 1), D * 2ull,
+                  static_cast<uint64_t>(shape.n_head) * D * 2, 64, g, kTileRows / g);
+        const uint64_t rows = static_cast<uint64_t>(shape.n_slots) * shape.chunk_size;
+        encode_3d(&m[1], p.k_pages, D, shape.n_kv_head, std::max<uint64_t>(rows, 1), D * 2ull,
+                  static_cast<uint64_t>(shape.n_kv_head) * D * 2, 64, 1, shape.chunk_size);
+        encode_3d(&m[2], p.v_pages, D, shape.n_kv_head, std::max<uint64_t>(rows, 1), D * 2ull,
+                  static_cast<uint64_t>(shape.n_kv_head) * D * 2, 64, 1, shape.chunk_size);
+        cache.q = p.q;
+        cache.k = p.k_pages;
+        cache.v = p.v_pages;
+        cache.total_tokens = total_tokens;
+        cache.valid = true;
+    }
+}
+
+void launch_attn_sm100(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens,
+                       cudaStream_t stream) {
+    if (p.n_items <= 0) return;
+    sm100_prepare_maps(p, shape, cache, total_tokens);
+    const int D = shape.head_size;
+    const auto* maps = reinterpret_cast<const CUtensorMap*>(cache.maps);
+    if (D == 128) launch_prefill<128>(p, maps, stream);
+    else launch_prefill<64>(p, maps, stream);
+}
+
+void sm100_cache_release(Sm100Cache& cache) { cache.valid = false; }
+
+} // namespace pb

@@ -26,5 +26,10 @@ int sm100_tile_tokens(int group);
 void launch_attn_sm100(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache,
                        int64_t total_tokens, cudaStream_t stream);
 void sm100_cache_release(Sm100Cache& cache);
+// (re)encodes the q / k / v tensor maps when pointers or sizes changed
+void sm100_prepare_maps(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens);
+bool decode_supports(int head_size, int chunk, int group);
+void launch_attn_decode(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens,
+                        cudaStream_t stream);
 
 } // namespace pb

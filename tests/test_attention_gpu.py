@@ -25,7 +25,7 @@ GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
 @pytest.fixture(scope="module")
 def gh(cuda):
-    import tests.gpu_helpers as gh
+    import gpu_helpers as gh
     return gh
 
 

@@ -84,7 +84,7 @@ def test_append_ragged_bf16_and_errors(cuda, oracle):
     torch = cuda
     shape = AttnShape(8, 2, 128, 16, 40, PB_BF16, 1.0)
     row = 2 * 128
-    spans = [(37, 20, [3, 7, 11]), (0, 1, [0]), (100, 29, [20, 21, 22, 23, 24, 25, 26, 27, 28])]
+    spans = [(37, 20, [3, 7, 11, 12]), (0, 1, [0]), (100, 29, [20, 21, 22, 23, 24, 25, 26, 27, 28])]
     total = sum(n for _, n, _ in spans)
     kr = torch.randn(total, row, device="cuda").to(torch.bfloat16)
     vr = torch.randn(total, row, device="cuda").to(torch.bfloat16)
