@@ -204,3 +204,89 @@ class Reference:
         a, b = _U64(), _U64()
         st = self.L.ref_model_bytes(preset.encode(), n_kv_override, chunk, ctypes.byref(a), ctypes.byref(b))
         return st, a.value, b.value
+
+
+class RefCache:
+    """The reference kvsim::PagedKvCache through the shim (raises RuntimeError(code))."""
+
+    class Err(RuntimeError):
+        def __init__(self, code):
+            super().__init__(f"reference status {code}")
+            self.code = code
+
+    def __init__(self, ref: "Reference", chunk, dev, host):
+        self.L = ref.L
+        self.h = self.L.ref_cache_create(chunk, dev, host)
+        assert self.h
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            self.L.ref_cache_destroy(self.h)
+            self.h = None
+
+    def _chk(self, st):
+        if st != 0:
+            raise RefCache.Err(st)
+
+    def allocate(self, conv, n, now):
+        out = np.zeros(max(1, n + 1), np.int64)
+        k = _I64()
+        self._chk(self.L.ref_cache_allocate(self.h, conv, n, now, _p(out), out.size, ctypes.byref(k)))
+        return out[: k.value].tolist()
+
+    def apply_evictions(self, ids, to_host):
+        ids = np.ascontiguousarray(ids, np.int64)
+        self._chk(self.L.ref_cache_evict(self.h, _p(ids) if len(ids) else None, len(ids), 1 if to_host else 0))
+
+    def _bring(self, kind, ids):
+        ids = np.ascontiguousarray(ids, np.int64)
+        slots = np.zeros(max(1, len(ids)), np.int32)
+        self._chk(self.L.ref_cache_bring_back(self.h, kind, _p(ids) if len(ids) else None, len(ids), _p(slots)))
+        return slots[: len(ids)].tolist()
+
+    def restore(self, ids):
+        return self._bring(0, ids)
+
+    def rematerialize(self, ids):
+        return self._bring(1, ids)
+
+    def release_conversation(self, conv):
+        self._chk(self.L.ref_cache_release(self.h, conv))
+
+    def retain_on_finish(self, conv, now):
+        self._chk(self.L.ref_cache_retain(self.h, conv, now))
+
+    def block_table(self, conv, ctx):
+        out = np.zeros(max(1, ctx + 1), np.int32)
+        k = _I64()
+        self._chk(self.L.ref_cache_block_table(self.h, conv, ctx, _p(out), out.size, ctypes.byref(k)))
+        return out[: k.value].tolist()
+
+    def counts(self):
+        c = np.zeros(8, np.int64)
+        self.L.ref_cache_counts(self.h, _p(c))
+        keys = ("device_capacity", "device_free", "device_reclaimable", "device_allocated", "host_capacity",
+                "host_free", "host_allocated", "verify_status")
+        return dict(zip(keys, (int(x) for x in c)))
+
+    def has_conversation(self, conv):
+        return bool(self.L.ref_cache_has(self.h, conv))
+
+    def total_tokens(self, conv):
+        return int(self.L.ref_cache_total_tokens(self.h, conv))
+
+    def append_chunks_needed(self, conv, add):
+        return int(self.L.ref_cache_append_needed(self.h, conv, add))
+
+    def conversation_chunks(self, conv):
+        n = 1 << 14
+        ids, kinds, slots = np.zeros(n, np.int64), np.zeros(n, np.int32), np.zeros(n, np.int32)
+        k = _I64()
+        self._chk(self.L.ref_cache_conv_chunks(self.h, conv, _p(ids), _p(kinds), _p(slots), n, ctypes.byref(k)))
+        return list(zip(ids[: k.value].tolist(), kinds[: k.value].tolist(), slots[: k.value].tolist()))
+
+    def dump(self):
+        n = self.L.ref_cache_dump(self.h, None, 0)
+        buf = ctypes.create_string_buffer(int(n) + 1)
+        self.L.ref_cache_dump(self.h, buf, n + 1)
+        return buf.value.decode()

@@ -276,3 +276,160 @@ def scatter_pages(staging: int, layer_stride: int, n_layers: int, page_bytes: in
 def fill_unit(dst: int, dtype: int, n: int, seed: int, first_draw: int,
               stream: Optional[int] = None) -> None:
     check(lib.pb_fill_splitmix_unit(dst, dtype, n, seed, first_draw, stream))
+
+
+# ============================================================================ KV bookkeeping
+class SlotMove(ctypes.Structure):
+    _fields_ = [("chunk", ctypes.c_int64), ("src_slot", ctypes.c_int32), ("dst_slot", ctypes.c_int32)]
+
+
+class ChunkRecord(ctypes.Structure):
+    _fields_ = [("chunk_id", ctypes.c_int64), ("conv_id", ctypes.c_int64), ("start_offset", ctypes.c_int64),
+                ("n_tokens", ctypes.c_int64), ("location", ctypes.c_int32), ("slot", ctypes.c_int32),
+                ("last_active", ctypes.c_double)]
+
+
+class LayoutSegment(ctypes.Structure):
+    _fields_ = [("kind", ctypes.c_int32), ("n_chunks", ctypes.c_int32), ("token_begin", ctypes.c_int64),
+                ("token_end", ctypes.c_int64), ("first_chunk", ctypes.c_int64)]
+
+
+DEVICE, HOST, DROPPED = 0, 1, 2
+
+_I64P = ctypes.POINTER(_I64)
+_CACHE_SIGS = {
+    "pb_cache_create": (_I32, [_I32, _I32, _I32, ctypes.POINTER(_P)]),
+    "pb_cache_destroy": (None, [_P]),
+    "pb_cache_allocate": (_I32, [_P, _I64, _I64, ctypes.c_double, _P, _I64, _I64P]),
+    "pb_cache_apply_evictions": (_I32, [_P, _P, _I64, _I32, _P]),
+    "pb_cache_restore": (_I32, [_P, _P, _I64, _P]),
+    "pb_cache_rematerialize": (_I32, [_P, _P, _I64, _P]),
+    "pb_cache_release_conversation": (_I32, [_P, _I64]),
+    "pb_cache_touch": (_I32, [_P, _I64, ctypes.c_double]),
+    "pb_cache_block_table": (_I32, [_P, _I64, _I64, _P, _I64, _I64P]),
+    "pb_cache_layout": (_I32, [_P, _I64, _P, _I64, _I64P, _I64P]),
+    "pb_cache_conversation_chunks": (_I32, [_P, _I64, _P, _I64, _I64P]),
+    "pb_cache_chunk": (_I32, [_P, _I64, _P]),
+    "pb_cache_collect_chunks": (_I32, [_P, _I32, _P, _I64, _P, _I64, _I64P]),
+    "pb_cache_counts": (None, [_P, _P]),
+    "pb_cache_has_conversation": (_I32, [_P, _I64]),
+    "pb_cache_total_tokens": (_I64, [_P, _I64]),
+    "pb_cache_append_chunks_needed": (_I32, [_P, _I64, _I64]),
+    "pb_cache_verify": (_I32, [_P]),
+    "pb_cache_dump": (_I64, [_P, ctypes.c_char_p, _I64]),
+}
+for _name, (_res, _args) in _CACHE_SIGS.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+_SIGS.update(_CACHE_SIGS)
+
+
+def _ids(ids) -> np.ndarray:
+    return np.ascontiguousarray(ids, dtype=np.int64)
+
+
+class KvCache:
+    """pb_kv_cache: the two-tier page-slot allocator (kvsim::PagedKvCache semantics)."""
+
+    def __init__(self, chunk_size: int, device_slots: int, host_slots: int):
+        h = _P()
+        check(lib.pb_cache_create(chunk_size, device_slots, host_slots, ctypes.byref(h)))
+        self._h = h
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.pb_cache_destroy(h)
+            self._h = None
+
+    def allocate(self, conv: int, n_tokens: int, now: float):
+        cap = max(1, n_tokens // 1 + 1)
+        out = np.zeros(min(cap, 1 << 20), np.int64)
+        n = _I64()
+        check(lib.pb_cache_allocate(self._h, conv, n_tokens, now, out.ctypes.data, out.size, ctypes.byref(n)))
+        return out[: n.value].tolist()
+
+    def _moves(self, fn, ids, *extra):
+        ids = _ids(ids)
+        moves = (SlotMove * max(1, len(ids)))()
+        check(fn(self._h, ids.ctypes.data if len(ids) else None, len(ids), *extra, moves))
+        return [(m.chunk, m.src_slot, m.dst_slot) for m in moves[: len(ids)]]
+
+    def apply_evictions(self, ids, to_host: bool):
+        ids = _ids(ids)
+        moves = (SlotMove * max(1, len(ids)))()
+        check(lib.pb_cache_apply_evictions(self._h, ids.ctypes.data if len(ids) else None, len(ids),
+                                           1 if to_host else 0, moves))
+        return [(m.chunk, m.src_slot, m.dst_slot) for m in moves[: len(ids)]]
+
+    def restore(self, ids):
+        return self._moves(lib.pb_cache_restore, ids)
+
+    def rematerialize(self, ids):
+        return self._moves(lib.pb_cache_rematerialize, ids)
+
+    def release_conversation(self, conv):
+        check(lib.pb_cache_release_conversation(self._h, conv))
+
+    def touch(self, conv, now):
+        check(lib.pb_cache_touch(self._h, conv, now))
+
+    retain_on_finish = touch
+
+    def block_table(self, conv, ctx):
+        out = np.zeros(max(1, ctx // 1 + 1), np.int32)
+        n = _I64()
+        check(lib.pb_cache_block_table(self._h, conv, ctx, out.ctypes.data, out.size, ctypes.byref(n)))
+        return out[: n.value].tolist()
+
+    def layout(self, conv):
+        segs = (LayoutSegment * 4096)()
+        n, total = _I64(), _I64()
+        check(lib.pb_cache_layout(self._h, conv, segs, 4096, ctypes.byref(n), ctypes.byref(total)))
+        return total.value, [(s.kind, s.token_begin, s.token_end, s.n_chunks) for s in segs[: n.value]]
+
+    def conversation_chunks(self, conv):
+        n = _I64()
+        check(lib.pb_cache_conversation_chunks(self._h, conv, None, 0, ctypes.byref(n)))
+        recs = (ChunkRecord * max(1, n.value))()
+        check(lib.pb_cache_conversation_chunks(self._h, conv, recs, n.value, ctypes.byref(n)))
+        return list(recs[: n.value])
+
+    def chunk(self, cid) -> ChunkRecord:
+        r = ChunkRecord()
+        check(lib.pb_cache_chunk(self._h, cid, ctypes.byref(r)))
+        return r
+
+    def collect_chunks(self, location, exclude=()):
+        ex = _ids(list(exclude) or [0])
+        out = np.zeros(1 << 16, np.int64)
+        n = _I64()
+        check(lib.pb_cache_collect_chunks(self._h, location, ex.ctypes.data, len(exclude), out.ctypes.data,
+                                          out.size, ctypes.byref(n)))
+        return out[: n.value].tolist()
+
+    def counts(self):
+        o = np.zeros(8, np.int64)
+        lib.pb_cache_counts(self._h, o.ctypes.data)
+        keys = ("device_capacity", "device_free", "device_reclaimable", "device_allocated", "host_capacity",
+                "host_free", "host_allocated", "chunk_size")
+        return dict(zip(keys, (int(x) for x in o)))
+
+    def has_conversation(self, conv) -> bool:
+        return bool(lib.pb_cache_has_conversation(self._h, conv))
+
+    def total_tokens(self, conv) -> int:
+        return int(lib.pb_cache_total_tokens(self._h, conv))
+
+    def append_chunks_needed(self, conv, add) -> int:
+        return int(lib.pb_cache_append_chunks_needed(self._h, conv, add))
+
+    def verify(self):
+        check(lib.pb_cache_verify(self._h))
+
+    def dump(self) -> str:
+        n = lib.pb_cache_dump(self._h, None, 0)
+        buf = ctypes.create_string_buffer(int(n) + 1)
+        lib.pb_cache_dump(self._h, buf, n + 1)
+        return buf.value.decode()
