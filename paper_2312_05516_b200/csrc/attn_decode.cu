@@ -124,9 +124,9 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2)
         const int pos0 = w.kv_begin + (warp + i * kDecWarps) * 16;
         const int valid_rows = min(16, w.kv_end - pos0);
         // ---- scores: lane (r, hh) dots its row's half with every query head ----
-        float sc[kMaxGroup];
+        float sc[kMaxGroup], sc2[kMaxGroup]; // two chains per head (latency, small groups)
 #pragma unroll
-        for (int j = 0; j < kMaxGroup; ++j) sc[j] = 0.f;
+        for (int j = 0; j < kMaxGroup; ++j) sc[j] = sc2[j] = 0.f;
 #pragma unroll
         for (int c = 0; c < kChunks; ++c) {
             // dims hh*(D/2) + c*8 .. +8 ; for D=128 that is half hh, 16B chunk c of the row
@@ -142,23 +142,25 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2)
                 if (j < g) {
                     const float4 qa = *reinterpret_cast<const float4*>(&s.q[j][d0]);
                     const float4 qb = *reinterpret_cast<const float4*>(&s.q[j][d0 + 4]);
-                    float t = sc[j];
+                    float t = sc[j], u = sc2[j];
                     t = fmaf(qa.x, k8[0], t);
-                    t = fmaf(qa.y, k8[1], t);
+                    u = fmaf(qa.y, k8[1], u);
                     t = fmaf(qa.z, k8[2], t);
-                    t = fmaf(qa.w, k8[3], t);
+                    u = fmaf(qa.w, k8[3], u);
                     t = fmaf(qb.x, k8[4], t);
-                    t = fmaf(qb.y, k8[5], t);
+                    u = fmaf(qb.y, k8[5], u);
                     t = fmaf(qb.z, k8[6], t);
-                    t = fmaf(qb.w, k8[7], t);
+                    u = fmaf(qb.w, k8[7], u);
                     sc[j] = t;
+                    sc2[j] = u;
                 }
             }
         }
 #pragma unroll
         for (int j = 0; j < kMaxGroup; ++j) {
             if (j < g) {
-                float x = sc[j] + __shfl_xor_sync(0xffffffffu, sc[j], 16);
+                float x = sc[j] + sc2[j];
+                x += __shfl_xor_sync(0xffffffffu, x, 16);
                 x = r < valid_rows ? x * sl2 : -CUDART_INF_F;
                 float mx = x;
                 mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));

@@ -221,24 +221,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_ld_wait();
                 tc_fence_before();
                 mbar_arrive(&s.s_empty[sb]);
-                // causal mask + running max (log2 domain)
+                // causal mask (only tiles that cross this row's boundary) + running max; eight
+                // independent max / sum chains keep the single warp per SMSP issuing
                 const int kv0 = j * kTileRows;
-                float mt = -CUDART_INF_F;
+                if (kv0 + kTileRows > allowed) {
 #pragma unroll
-                for (int c = 0; c < 128; ++c) {
-                    const float v = (kv0 + c < allowed) ? x[c] * sl2 : -CUDART_INF_F;
-                    x[c] = v;
-                    mt = fmaxf(mt, v);
+                    for (int c = 0; c < 128; ++c) x[c] = (kv0 + c < allowed) ? x[c] : -CUDART_INF_F;
                 }
+                float pm[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) pm[u] = x[u];
+#pragma unroll
+                for (int c = 8; c < 128; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
+                const float mt = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                                       fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * sl2;
                 const bool grow = mt > m_run + kRescaleThreshold;
                 const float m_new = grow ? mt : m_run;
                 const float corr = grow ? ex2(m_run - m_new) : 1.f;
-                float sum = 0.f;
+                float ps[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) ps[u] = 0.f;
 #pragma unroll
                 for (int c = 0; c < 128; ++c) {
-                    x[c] = ex2(x[c] - m_new);
-                    sum += x[c];
+                    x[c] = ex2(fmaf(x[c], sl2, -m_new)); // exp((s - max) / scale) in base 2
+                    ps[c & 7] += x[c];
                 }
+                const float sum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
                 l_run = l_run * corr + sum;
                 m_run = m_new;
                 if (j > 0) {
