@@ -63,7 +63,8 @@ __global__ void __launch_bounds__(kDecWarps * 32, 2)
     constexpr int kChunks = D / 16;  // 16B chunks per half-row handled by one lane (D/2 dims)
     constexpr int kDimsPerLane = D / 32;
     extern __shared__ uint8_t smem_raw[];
-    DecSmem<D, kMaxGroup>& s = *reinterpret_cast<DecSmem<D, kMaxGroup>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    // align with pointer arithmetic on the __shared__ array so loads stay LDS (not generic LD)
+    DecSmem<D, kMaxGroup>& s = *reinterpret_cast<DecSmem<D, kMaxGroup>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
     const WorkItem w = p.items[blockIdx.x];

@@ -4,19 +4,23 @@
 // Semantics: paged_multi_token_attention, /root/reference/proj/src/attention.cpp:73-132
 // (token i of a span sees [0, causal_offset+i], head h reads kv head h/group, softmax with
 // max subtraction).  B200 design:
-//   * one work item = (span, kv head, block of 128/group query tokens); the GQA group is packed
-//     into the M dimension, so M = 128 rows = tokens x heads-of-the-group (PAPER.md:708-717
-//     fuses QK^T, mask, softmax, PV in one kernel; here on tcgen05 with TMEM accumulators);
-//   * persistent CTAs, 6 warps: warp 0 = TMA producer, warp 1 = MMA issuer (single elected
-//     thread, tcgen05.mma.cta_group::1.kind::f16, accumulators in TMEM), warps 2-5 =
-//     softmax / correction / epilogue, one TMEM lane (= one query row) per thread;
+//   * one work item = (span, kv head, block of 2 x 128/group query tokens) = two M=128 query
+//     tiles A and B that share every K/V tile loaded; the GQA group is packed into M
+//     (rows = tokens x heads-of-the-group), PAPER.md:708-717 fuses QK^T, mask, softmax, PV;
+//   * persistent CTAs, 3 warpgroups: WG0 / WG1 = softmax + correction + epilogue of query
+//     tiles A / B (one TMEM lane = one query row per thread, 224 registers via setmaxnreg),
+//     WG2 = warp 8 TMA producer + warp 9 MMA issuer (one elected thread,
+//     tcgen05.mma.cta_group::1.kind::f16) at 56 registers;
+//   * TMEM: S_A | S_B | O_A | O_B (4 x 128 columns).  P (bf16) is written back over S with
+//     tcgen05.st and fed to the PV MMA straight from TMEM (A operand in TMEM), so P never
+//     touches shared memory;
+//   * MMA order per KV tile j: PV_A(j), S_A(j+1), PV_B(j), S_B(j+1): while one softmax group
+//     works on its scores the tensor core runs the other group's two MMAs (ping-pong);
 //   * KV pages are gathered straight from the paged pools by TMA: a 128-row KV tile is
 //     128/page_tokens box loads {64 dims, 1 kv head, page_tokens rows} at row coordinate
 //     block_table[p] * page_tokens (SWIZZLE_128B); pages past the span's table are fetched
 //     out of bounds, which TMA zero-fills;
-//   * S = Q K^T double-buffered in TMEM (S_{j+1} is issued before P_j V_j), P written to
-//     shared memory in the UMMA K-major SW128 layout, O accumulated in TMEM, rescaled lazily
-//     (only when the running max grows by more than 2^8).
+//   * O is rescaled lazily (only when a row's running max grows by more than 2^8).
 #include "attn_internal.hpp"
 #include "pb_common.hpp"
 #include "sm100_attn.hpp"
@@ -36,26 +40,53 @@ namespace {
 
 using namespace pb::sm100;
 
-constexpr int kThreads = 192;
-constexpr int kTileRows = 128;       // M rows per work item and kv rows per tile
-constexpr uint32_t kTmemCols = 512;  // S0 [0,128) S1 [128,256) O [256, 256+D)
+constexpr int kThreads = 384; // WG0/WG1 softmax of tiles A/B, WG2: TMA warp, MMA warp, 2 spare
+constexpr int kTileRows = 128;        // M rows per query tile and kv rows per kv tile
+constexpr uint32_t kTmemCols = 512;   // S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
 constexpr uint32_t kColO = 256;
+constexpr bool kUseSetMaxNReg = false;
 constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max grows by > 2^8
 
 template <int D>
 struct __align__(1024) Smem {
-    uint8_t q[kTileRows * D * 2];     // [D/64][128 rows][128 B] K-major SW128
+    uint8_t q[2][kTileRows * D * 2];  // tiles A, B: [D/64][128 rows][128 B] K-major SW128
     uint8_t k[2][kTileRows * D * 2];  // 2-stage ring, same layout
     uint8_t v[2][kTileRows * D * 2];  // 2-stage ring; read as MN-major SW128 B operand
-    uint8_t p[kTileRows * kTileRows * 2]; // [2 kv halves][128 rows][128 B]
     uint64_t q_full, q_empty;
     uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-    uint64_t s_full[2], s_empty[2];
-    uint64_t p_full, o_ready, o_empty;
+    uint64_t s_full[2], p_full[2], o_ready[2], o_empty[2]; // per query tile
     uint32_t tmem_base;
 };
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
+
+// Query-tile geometry of one work item.
+struct ItemTiles {
+    int nt[2];     // query tokens in tile A / B (B may be empty)
+    int ntiles[2]; // kv tiles each query tile needs (0 when empty)
+    int n_kv;      // kv tiles loaded for the item
+};
+
+__device__ __forceinline__ ItemTiles item_tiles(const WorkItem& w, const SpanDev& sp, int tpt) {
+    ItemTiles r;
+    r.nt[0] = min(w.nt, tpt);
+    r.nt[1] = w.nt - r.nt[0];
+    r.ntiles[0] = ceil_div(sp.causal_offset + w.t0 + r.nt[0], kTileRows);
+    r.ntiles[1] = r.nt[1] > 0 ? ceil_div(sp.causal_offset + w.t0 + w.nt, kTileRows) : 0;
+    r.n_kv = max(r.ntiles[0], r.ntiles[1]);
+    return r;
+}
+
+// A operand in TMEM (P, bf16), B from shared memory (V).
+__device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
+                                             uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "r"(a_tmem), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -65,11 +96,10 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t kHalfBytes = kTileRows * 128;
     constexpr uint32_t kTileBytes = kTileRows * D * 2;
     extern __shared__ uint8_t smem_raw[];
-    Smem<D>& s = *reinterpret_cast<Smem<D>*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    Smem<D>& s = *reinterpret_cast<Smem<D>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
     const int g = p.group;
-    const int tpt = kTileRows / g;         // query tokens per tile
+    const int tpt = kTileRows / g;         // query tokens per query tile
     const int chunk = p.chunk;
     const int ppt = kTileRows / chunk;     // pages per kv tile
 
@@ -82,23 +112,25 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&s.v_full[i], 1);
             mbar_init(&s.v_empty[i], 1);
             mbar_init(&s.s_full[i], 1);
-            mbar_init(&s.s_empty[i], 128);
+            mbar_init(&s.p_full[i], 128);
+            mbar_init(&s.o_ready[i], 1);
+            mbar_init(&s.o_empty[i], 128);
         }
-        mbar_init(&s.p_full, 128);
-        mbar_init(&s.o_ready, 1);
-        mbar_init(&s.o_empty, 128);
         mbar_fence_init();
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
     }
-    if (warp == 1) tmem_alloc<kTmemCols>(&s.tmem_base);
+    if (warp == 9) tmem_alloc<kTmemCols>(&s.tmem_base);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = s.tmem_base;
+    const int wg = warp >> 2;
+    if (kUseSetMaxNReg && wg == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 112;" ::: "memory");
+    else if (kUseSetMaxNReg) asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
 
-    if (warp == 0) {
+    if (warp == 8) {
         // ============================ TMA producer ============================
         if (elect_one()) {
             int it = 0, kst = 0, vst = 0;
@@ -108,13 +140,16 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
                 const WorkItem w = p.items[item];
                 const SpanDev sp = p.spans[w.span];
+                const ItemTiles T = item_tiles(w, sp, tpt);
                 const int32_t* table = p.block_tables + sp.bt_off;
-                const int n_tiles = ceil_div(sp.causal_offset + w.t0 + w.nt, kTileRows);
                 if (it > 0) mbar_wait(&s.q_empty, (it - 1) & 1);
-                mbar_arrive_expect_tx(&s.q_full, q_bytes);
-                for (int h = 0; h < KH; ++h)
-                    tma_load_3d(s.q + h * kHalfBytes, &tm_q, &s.q_full, h * 64, w.kvh * g, sp.query_start + w.t0);
-                for (int j = 0; j < n_tiles; ++j) {
+                mbar_arrive_expect_tx(&s.q_full, q_bytes * (T.nt[1] > 0 ? 2u : 1u));
+                for (int t = 0; t < 2; ++t)
+                    if (T.nt[t] > 0)
+                        for (int h = 0; h < KH; ++h)
+                            tma_load_3d(s.q[t] + h * kHalfBytes, &tm_q, &s.q_full, h * 64, w.kvh * g,
+                                        sp.query_start + w.t0 + t * tpt);
+                for (int j = 0; j < T.n_kv; ++j) {
                     for (int which = 0; which < 2; ++which) {
                         uint64_t* full = which ? &s.v_full[vst] : &s.k_full[kst];
                         uint64_t* empty = which ? &s.v_empty[vst] : &s.k_empty[kst];
@@ -137,92 +172,112 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp == 1) {
+    } else if (warp == 9) {
         // ============================ MMA issuer =============================
         if (elect_one()) {
             constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
             constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
-            const uint32_t q_addr = smem_u32(s.q);
-            const uint32_t p_addr = smem_u32(s.p);
             int it = 0, kst = 0, vst = 0;
-            uint32_t kph = 0, vph = 0, n_s = 0, n_p = 0;
+            uint32_t kph = 0, vph = 0;
+            uint32_t n_p[2] = {0, 0}, n_oe[2] = {0, 0};
             for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
                 const WorkItem w = p.items[item];
                 const SpanDev sp = p.spans[w.span];
-                const int n_tiles = ceil_div(sp.causal_offset + w.t0 + w.nt, kTileRows);
+                const ItemTiles T = item_tiles(w, sp, tpt);
                 mbar_wait(&s.q_full, it & 1);
                 tc_fence_after();
-                auto issue_s = [&]() {
-                    const uint32_t sb = n_s & 1;
-                    mbar_wait(&s.k_full[kst], kph);
-                    mbar_wait(&s.s_empty[sb], ((n_s >> 1) & 1) ^ 1);
-                    tc_fence_after();
-                    const uint32_t k_addr = smem_u32(s.k[kst]);
+                // S_t = Q_t K^T for the kv tile in stage kst
+                // descriptors are advanced by adding (byte offset >> 4) to the start-address
+                // field (no carry: shared addresses < 256 KB), which keeps register use low
+                auto issue_s = [&](int t) {
+                    const uint64_t qd = umma_desc_sw128(smem_u32(s.q[t]), 16, 1024);
+                    const uint64_t kd = umma_desc_sw128(smem_u32(s.k[kst]), 16, 1024);
 #pragma unroll
                     for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-                        umma_bf16_ss(tmem + sb * 128, umma_desc_sw128(q_addr + off, 16, 1024),
-                                     umma_desc_sw128(k_addr + off, 16, 1024), idesc_s, kk > 0);
+                        const uint32_t off = ((kk >> 2) * kHalfBytes + (kk & 3) * 32) >> 4;
+                        umma_bf16_ss(tmem + t * 128, qd + off, kd + off, idesc_s, kk > 0);
                     }
-                    umma_commit(&s.k_empty[kst]);
-                    umma_commit(&s.s_full[sb]);
-                    if (++kst == 2) { kst = 0; kph ^= 1; }
-                    ++n_s;
+                    umma_commit(&s.s_full[t]);
                 };
-                issue_s();
-                if (n_tiles > 1) issue_s();
-                for (int j = 0; j < n_tiles; ++j) {
-                    mbar_wait(&s.p_full, n_p & 1);
-                    ++n_p;
-                    if (j == 0) mbar_wait(&s.o_empty, (it & 1) ^ 1);
+                // S for kv tile 0
+                mbar_wait(&s.k_full[kst], kph);
+                tc_fence_after();
+                for (int t = 0; t < 2; ++t)
+                    if (T.ntiles[t] > 0) issue_s(t);
+                umma_commit(&s.k_empty[kst]);
+                if (++kst == 2) { kst = 0; kph ^= 1; }
+                for (int j = 0; j < T.n_kv; ++j) {
                     mbar_wait(&s.v_full[vst], vph);
-                    tc_fence_after();
-                    const uint32_t v_addr = smem_u32(s.v[vst]);
+                    bool k_next_ready = false;
+                    for (int t = 0; t < 2; ++t) {
+                        if (j >= T.ntiles[t]) continue;
+                        mbar_wait(&s.p_full[t], n_p[t] & 1);
+                        ++n_p[t];
+                        if (j == 0) {
+                            mbar_wait(&s.o_empty[t], (n_oe[t] & 1) ^ 1);
+                            ++n_oe[t];
+                        }
+                        tc_fence_after();
+                        const uint64_t vd = umma_desc_sw128(smem_u32(s.v[vst]), kHalfBytes, 1024);
 #pragma unroll
-                    for (int kk = 0; kk < kTileRows / 16; ++kk) {
-                        const uint32_t a_off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-                        umma_bf16_ss(tmem + kColO, umma_desc_sw128(p_addr + a_off, 16, 1024),
-                                     umma_desc_sw128(v_addr + kk * 2048, kHalfBytes, 1024), idesc_o,
-                                     (j > 0 || kk > 0) ? 1u : 0u);
+                        for (int kk = 0; kk < kTileRows / 16; ++kk)
+                            umma_bf16_ts(tmem + kColO + t * 128, tmem + t * 128 + kk * 8, vd + kk * (2048 >> 4),
+                                         idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+                        if (j + 1 == T.ntiles[t]) umma_commit(&s.o_ready[t]);
+                        if (j + 1 < T.ntiles[t]) {
+                            if (!k_next_ready) {
+                                mbar_wait(&s.k_full[kst], kph);
+                                tc_fence_after();
+                                k_next_ready = true;
+                            }
+                            issue_s(t);
+                        }
                     }
                     umma_commit(&s.v_empty[vst]);
-                    umma_commit(&s.o_ready);
                     if (++vst == 2) { vst = 0; vph ^= 1; }
-                    if (j + 2 < n_tiles) issue_s();
+                    if (j + 1 < T.n_kv) {
+                        if (!k_next_ready) { // no query tile needed it (cannot happen; keep rings in step)
+                            mbar_wait(&s.k_full[kst], kph);
+                        }
+                        umma_commit(&s.k_empty[kst]);
+                        if (++kst == 2) { kst = 0; kph ^= 1; }
+                    }
                 }
                 umma_commit(&s.q_empty);
             }
         }
-    } else {
-        // ===================== softmax / correction / epilogue =====================
-        const int quad = warp & 3;                 // TMEM lane quadrant of this warp
-        const int row = quad * 32 + lane;          // query row of this thread
+    } else if (wg < 2) {
+        // ============ softmax / correction / epilogue (one group per query tile) ============
+        const int t = wg;                           // query tile of this warpgroup
+        const int quad = warp & 3;                  // TMEM lane quadrant of this warp
+        const int row = quad * 32 + (threadIdx.x & 31);
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+        const uint32_t col_s = t * 128;
+        const uint32_t col_o = kColO + t * 128;
         const float sl2 = p.scale_log2;
         uint32_t n_s = 0, n_o = 0;
-        int it = 0;
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
-        for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+        for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
             const WorkItem w = p.items[item];
             const SpanDev sp = p.spans[w.span];
-            const int n_tiles = ceil_div(sp.causal_offset + w.t0 + w.nt, kTileRows);
+            const ItemTiles T = item_tiles(w, sp, tpt);
+            const int n_tiles = T.ntiles[t];
+            if (n_tiles == 0) continue;
             const int t_local = row / g;
-            const bool valid = t_local < w.nt && row < g * tpt;
-            const int allowed = sp.causal_offset + w.t0 + (valid ? t_local : 0) + 1;
+            const bool valid = t_local < T.nt[t] && row < g * tpt;
+            const int tok0 = w.t0 + t * tpt;           // first span-relative token of this tile
+            const int allowed = sp.causal_offset + tok0 + (valid ? t_local : 0) + 1;
             float m_run = -CUDART_INF_F, l_run = 0.f;
             for (int j = 0; j < n_tiles; ++j) {
-                const uint32_t sb = n_s & 1;
-                mbar_wait(&s.s_full[sb], (n_s >> 1) & 1);
+                mbar_wait(&s.s_full[t], n_s & 1);
                 ++n_s;
                 tc_fence_after();
                 float x[128];
 #pragma unroll
-                for (int c = 0; c < 4; ++c) tmem_ld32(t_lane + sb * 128 + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
+                for (int c = 0; c < 4; ++c)
+                    tmem_ld32(t_lane + col_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
                 tmem_ld_wait();
-                tc_fence_before();
-                mbar_arrive(&s.s_empty[sb]);
-                // causal mask (only tiles that cross this row's boundary) + running max; eight
-                // independent max / sum chains keep the single warp per SMSP issuing
+                // causal mask (only tiles that cross this row's boundary) + running max
                 const int kv0 = j * kTileRows;
                 if (kv0 + kTileRows > allowed) {
 #pragma unroll
@@ -241,60 +296,53 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float ps[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) ps[u] = 0.f;
+                uint32_t pk0[32], pk1[32];
 #pragma unroll
-                for (int c = 0; c < 128; ++c) {
-                    x[c] = ex2(fmaf(x[c], sl2, -m_new)); // exp((s - max) / scale) in base 2
-                    ps[c & 7] += x[c];
+                for (int c = 0; c < 128; c += 2) {
+                    // exp((s - max) / scale) in base 2; one pair in four on the FMA pipe (cubic),
+                    // the rest on MUFU, so the two softmax groups do not saturate MUFU
+                    const float a0 = fmaf(x[c], sl2, -m_new), a1 = fmaf(x[c + 1], sl2, -m_new);
+                    const bool poly = ((c >> 1) & 3) == 3;
+                    const float e0 = poly ? exp2_poly3(a0) : ex2(a0);
+                    const float e1 = poly ? exp2_poly3(a1) : ex2(a1);
+                    ps[c & 7] += e0;
+                    ps[(c + 1) & 7] += e1;
+                    if (c < 64) pk0[c >> 1] = pack_bf16x2(e0, e1);
+                    else pk1[(c - 64) >> 1] = pack_bf16x2(e0, e1);
+                    if (c == 62) tmem_st32(t_lane + col_s, pk0); // P over the first 64 columns of S_t
                 }
+                tmem_st32(t_lane + col_s + 32, pk1);
                 const float sum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
                 l_run = l_run * corr + sum;
                 m_run = m_new;
-                if (j > 0) {
-                    // P_{j-1} V_{j-1} must be done before O is rescaled and P is overwritten
-                    mbar_wait(&s.o_ready, n_o & 1);
-                    ++n_o;
-                    tc_fence_after();
-                    if (__any_sync(0xffffffffu, grow)) {
+                // S_t(j) landing implies PV_t(j-1) completed (in-order tensor pipe, the commit for
+                // s_full was issued after it): O_t may be rescaled (after P, to keep registers low)
+                if (j > 0 && __any_sync(0xffffffffu, grow)) {
 #pragma unroll
-                        for (int c = 0; c < D / 32; ++c) {
-                            uint32_t o[32];
-                            tmem_ld32(t_lane + kColO + c * 32, o);
-                            tmem_ld_wait();
+                    for (int c = 0; c < D / 32; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(t_lane + col_o + c * 32, o);
+                        tmem_ld_wait();
 #pragma unroll
-                            for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-                            tmem_st32(t_lane + kColO + c * 32, o);
-                        }
-                        tmem_st_wait();
+                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+                        tmem_st32(t_lane + col_o + c * 32, o);
                     }
                 }
-                // P (bf16) -> shared memory, UMMA K-major SW128: [kv half][row][128 B]
-                uint8_t* prow = s.p + (row >> 3) * 1024 + (row & 7) * 128;
-#pragma unroll
-                for (int cc = 0; cc < 16; ++cc) {
-                    const int kb = cc >> 3, c8 = cc & 7;
-                    uint4 v;
-                    v.x = pack_bf16x2(x[cc * 8 + 0], x[cc * 8 + 1]);
-                    v.y = pack_bf16x2(x[cc * 8 + 2], x[cc * 8 + 3]);
-                    v.z = pack_bf16x2(x[cc * 8 + 4], x[cc * 8 + 5]);
-                    v.w = pack_bf16x2(x[cc * 8 + 6], x[cc * 8 + 7]);
-                    *reinterpret_cast<uint4*>(prow + kb * kHalfBytes + ((c8 ^ (row & 7)) << 4)) = v;
-                }
-                fence_proxy_async_smem();
+                tmem_st_wait();
                 tc_fence_before();
-                mbar_arrive(&s.p_full);
+                mbar_arrive(&s.p_full[t]);
             }
             // epilogue: O / l -> bf16 -> global
-            mbar_wait(&s.o_ready, n_o & 1);
+            mbar_wait(&s.o_ready[t], n_o & 1);
             ++n_o;
             tc_fence_after();
             const float inv_l = 1.f / l_run;
             const int h = w.kvh * g + (row % g);
-            __nv_bfloat16* orow =
-                out + (static_cast<size_t>(sp.query_start + w.t0 + t_local) * p.n_head + h) * D;
+            __nv_bfloat16* orow = out + (static_cast<size_t>(sp.query_start + tok0 + t_local) * p.n_head + h) * D;
 #pragma unroll
             for (int c = 0; c < D / 32; ++c) {
                 uint32_t o[32];
-                tmem_ld32(t_lane + kColO + c * 32, o);
+                tmem_ld32(t_lane + col_o + c * 32, o);
                 tmem_ld_wait();
                 if (valid) {
 #pragma unroll
@@ -309,12 +357,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
             tc_fence_before();
-            mbar_arrive(&s.o_empty);
+            mbar_arrive(&s.o_empty[t]);
         }
     }
     tc_fence_before();
     __syncthreads();
-    if (warp == 1) {
+    if (warp == 9) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem);
     }
@@ -377,7 +425,7 @@ bool sm100_supports(int head_size, int chunk, int group) {
            group >= 1 && group <= 128;
 }
 
-int sm100_tile_tokens(int group) { return kTileRows / group; }
+int sm100_tile_tokens(int group) { return 2 * (kTileRows / group); } // two query tiles per item
 
 void sm100_prepare_maps(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens) {
     const int D = shape.head_size;
