@@ -1,18 +1,21 @@
 // Single-token (decode) spans: memory-bound split-KV SIMT path.
 //
 // Semantics: single_token_attention, /root/reference/proj/src/attention.cpp:134-188 (one
-// query row per head against the whole context; the same as the multi-token path with
+// query row per head against the whole context; identical to the multi-token path with
 // q_len = 1).  B200 design:
-//   * one work item = (span, kv head, page range); long contexts are split across CTAs and
-//     the partial (max, sum, unnormalised O) of each split is merged inside the same launch by
+//   * one work unit = (span, kv head, page range of <= 64 pages); long contexts are split and
+//     the partial (max, sum, unnormalised O) of each split is merged in the same launch by
 //     the last-arriving split (atomic ticket, self-resetting);
-//   * all `group` query heads of the kv head are served by the same K/V bytes (each KV byte is
-//     read from HBM once);
-//   * each of the 4 warps owns a private 3-stage ring of pages in shared memory, filled by TMA
-//     ({64 dims, 1 kv head, 16 rows} boxes, SWIZZLE_128B => conflict-free row reads), and
-//     walks pages w, w+4, ...; the 4 warps' partials are merged through shared memory;
-//   * scores: lane = (row, 64-dim half), halves combined with one shuffle, page max with
-//     4 xor-shuffles per head; P broadcast through shared memory; lanes own 4 (or 2) output
+//   * all `group` query heads of the kv head are served by the same K/V bytes;
+//   * persistent CTAs; every WARP is an independent streaming engine: it pulls units from a
+//     global atomic queue (work stealing, units sorted longest-first) and keeps a private
+//     3-stage ring of 16-token pages filled by TMA ({64 dims, 1 kv head, 16 rows} boxes,
+//     SWIZZLE_128B, so row reads are bank-conflict free) that runs ahead ACROSS unit
+//     boundaries — no per-unit pipeline start-up, no cross-warp merge;
+//   * the unit's q rows (bf16, contiguous) arrive by cp.async.bulk on their own barrier,
+//     issued together with the unit's first page;
+//   * scores: lane = (page row, half of the dims), halves combined with one shuffle, page max
+//     with 4 xor-shuffles per head; P broadcast through shared memory; lanes own D/32 output
 //     dims for the PV update.
 #include "attn_internal.hpp"
 #include "pb_common.hpp"
@@ -31,262 +34,340 @@ namespace {
 
 using namespace pb::sm100;
 
-constexpr int kDecWarps = 4;
 constexpr int kDecStages = 3;
 constexpr int kMaxGroup = 16;
 
+__host__ __device__ constexpr int dec_warps(int G) { return G <= 8 ? 6 : 4; }
+
 template <int D, int G>
-struct __align__(1024) DecSmem {
-    static constexpr int KH = D / 64 > 0 ? D / 64 : 1;
-    static constexpr int kPageBytes = 16 * D * 2;             // one kv head, 16 rows
-    static_assert(G * D * 4 <= kDecStages * 2 * kPageBytes, "merge buffer aliases the warp's ring");
-    // [warp][stage][K|V][half][row][128B]; after the page loop each warp's ring is reused
-    // as its fp32 O partial [G][D] for the cross-warp merge
-    uint8_t kv[kDecWarps][kDecStages][2][kPageBytes];
-    float q[G][D];                                            // query rows (fp32)
-    float pbuf[kDecWarps][G][16];                             // per-warp page probabilities
-    float m[kDecWarps][G];
-    float l[kDecWarps][G];
-    uint64_t full[kDecWarps][kDecStages];
-    int last;
-    __device__ float* o(int warp) { return reinterpret_cast<float*>(kv[warp][0][0]); }
+struct __align__(1024) DecWarp {
+    static constexpr int KH = D / 64;
+    static constexpr int kPageBytes = 16 * D * 2;        // one kv head, 16 rows
+    uint8_t page[kDecStages][2][kPageBytes];             // [stage][K|V][half][row][128 B]
+    uint8_t qraw[kDecStages][G * D * 2];                 // bf16 q rows, slot = unit seq % stages
+    float q[G][D];                                       // fp32 q of the unit being consumed
+    float pbuf[G][16];                                   // page probabilities
+    uint64_t full[kDecStages];
+    uint64_t qfull[kDecStages];
 };
 
 __device__ __forceinline__ float bf_lo(uint32_t x) { return __uint_as_float(x << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t x) { return __uint_as_float(x & 0xffff0000u); }
 
-template <int D, int kMaxGroup>
-__global__ void __launch_bounds__(kDecWarps * 32, 2)
-    attn_decode_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
-                       const AttnParams p) {
-    constexpr int KH = DecSmem<D, kMaxGroup>::KH;
-    constexpr int kChunks = D / 16;  // 16B chunks per half-row handled by one lane (D/2 dims)
-    constexpr int kDimsPerLane = D / 32;
-    extern __shared__ uint8_t smem_raw[];
-    // align with pointer arithmetic on the __shared__ array so loads stay LDS (not generic LD)
-    DecSmem<D, kMaxGroup>& s = *reinterpret_cast<DecSmem<D, kMaxGroup>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
-    const int warp = threadIdx.x >> 5;
-    const int lane = threadIdx.x & 31;
-    const WorkItem w = p.items[blockIdx.x];
-    const SpanDev sp = p.spans[w.span];
-    const int g = p.group;
-    const int32_t* table = p.block_tables + sp.bt_off;
-    const int page0 = w.kv_begin >> 4;
-    const int n_pages = (w.kv_end - w.kv_begin + 15) >> 4;
-    const float sl2 = p.scale_log2;
-
-    if (lane == 0) {
-        for (int st = 0; st < kDecStages; ++st) mbar_init(&s.full[warp][st], 1);
-        mbar_fence_init();
-    }
-    // query rows of the group, fp32
-    {
-        const __nv_bfloat16* q = static_cast<const __nv_bfloat16*>(p.q) +
-                                 (static_cast<size_t>(sp.query_start) * p.n_head + static_cast<size_t>(w.kvh) * g) * D;
-        for (int e = threadIdx.x; e < g * D; e += blockDim.x) s.q[e / D][e % D] = __bfloat162float(q[e]);
-    }
-    __syncthreads();
-
-    // ---- per-warp page ring ----
-    const uint32_t page_tx = 2u * KH * 16u * 128u;
-    auto issue = [&](int local_page, int stage) {
-        const int row = table[page0 + local_page] * 16;
-        uint8_t* dst = s.kv[warp][stage][0];
-        mbar_arrive_expect_tx(&s.full[warp][stage], page_tx);
-        for (int h = 0; h < KH; ++h) {
-            tma_load_3d(dst + h * 2048, &tm_k, &s.full[warp][stage], h * 64, w.kvh, row);
-            tma_load_3d(dst + DecSmem<D, kMaxGroup>::kPageBytes + h * 2048, &tm_v, &s.full[warp][stage], h * 64, w.kvh, row);
-        }
-    };
-    int my_pages = 0;
-    for (int lp = warp; lp < n_pages; lp += kDecWarps) ++my_pages;
-    if (lane == 0)
-        for (int i = 0; i < kDecStages - 1 && i < my_pages; ++i) issue(warp + i * kDecWarps, i);
-
-    float m_run[kMaxGroup], l_lane[kMaxGroup], acc[kMaxGroup][kDimsPerLane];
-#pragma unroll
-    for (int j = 0; j < kMaxGroup; ++j) {
-        m_run[j] = -CUDART_INF_F;
-        l_lane[j] = 0.f;
-#pragma unroll
-        for (int e = 0; e < kDimsPerLane; ++e) acc[j][e] = 0.f;
-    }
-    const int r = lane & 15;        // page row scored by this lane
-    const int hh = lane >> 4;       // which half of the dims
-    for (int i = 0; i < my_pages; ++i) {
-        const int stage = i % kDecStages;
-        if (lane == 0 && i + kDecStages - 1 < my_pages) {
-            fence_proxy_async_smem();
-            issue(warp + (i + kDecStages - 1) * kDecWarps, (i + kDecStages - 1) % kDecStages);
-        }
-        mbar_wait(&s.full[warp][stage], (i / kDecStages) & 1);
-        const uint8_t* kpg = s.kv[warp][stage][0];
-        const uint8_t* vpg = s.kv[warp][stage][1];
-        const int pos0 = w.kv_begin + (warp + i * kDecWarps) * 16;
-        const int valid_rows = min(16, w.kv_end - pos0);
-        // ---- scores: lane (r, hh) dots its row's half with every query head ----
-        float sc[kMaxGroup], sc2[kMaxGroup]; // two chains per head (latency, small groups)
-#pragma unroll
-        for (int j = 0; j < kMaxGroup; ++j) sc[j] = sc2[j] = 0.f;
-#pragma unroll
-        for (int c = 0; c < kChunks; ++c) {
-            // dims hh*(D/2) + c*8 .. +8 ; for D=128 that is half hh, 16B chunk c of the row
-            int half, cin;
-            if (D == 128) { half = hh; cin = c; }
-            else { half = 0; cin = hh * (kChunks) + c; }
-            const uint4 kv4 = *reinterpret_cast<const uint4*>(kpg + half * 2048 + r * 128 + ((cin ^ (r & 7)) << 4));
-            const float k8[8] = {bf_lo(kv4.x), bf_hi(kv4.x), bf_lo(kv4.y), bf_hi(kv4.y),
-                                 bf_lo(kv4.z), bf_hi(kv4.z), bf_lo(kv4.w), bf_hi(kv4.w)};
-            const int d0 = hh * (D / 2) + c * 8;
-#pragma unroll
-            for (int j = 0; j < kMaxGroup; ++j) {
-                if (j < g) {
-                    const float4 qa = *reinterpret_cast<const float4*>(&s.q[j][d0]);
-                    const float4 qb = *reinterpret_cast<const float4*>(&s.q[j][d0 + 4]);
-                    float t = sc[j], u = sc2[j];
-                    t = fmaf(qa.x, k8[0], t);
-                    u = fmaf(qa.y, k8[1], u);
-                    t = fmaf(qa.z, k8[2], t);
-                    u = fmaf(qa.w, k8[3], u);
-                    t = fmaf(qb.x, k8[4], t);
-                    u = fmaf(qb.y, k8[5], u);
-                    t = fmaf(qb.z, k8[6], t);
-                    u = fmaf(qb.w, k8[7], u);
-                    sc[j] = t;
-                    sc2[j] = u;
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < kMaxGroup; ++j) {
-            if (j < g) {
-                float x = sc[j] + sc2[j];
-                x += __shfl_xor_sync(0xffffffffu, x, 16);
-                x = r < valid_rows ? x * sl2 : -CUDART_INF_F;
-                float mx = x;
-                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
-                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
-                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
-                mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
-                const float m_new = fmaxf(m_run[j], mx);
-                const float corr = ex2(m_run[j] - m_new);
-                const float pr = ex2(x - m_new);
-                m_run[j] = m_new;
-                l_lane[j] = l_lane[j] * corr + (hh == 0 ? pr : 0.f);
-#pragma unroll
-                for (int e = 0; e < kDimsPerLane; ++e) acc[j][e] *= corr;
-                if (hh == 0) s.pbuf[warp][j][r] = pr;
-            }
-        }
-        __syncwarp();
-        // ---- PV: lane owns dims [lane*kDimsPerLane, +kDimsPerLane) ----
-        const int vh = (D == 128) ? (lane >> 4) : 0;
-        const int vbyte = (D == 128) ? ((lane & 15) * 8) : (lane * 4); // byte offset inside the 128 B row
-#pragma unroll
-        for (int rr = 0; rr < 16; ++rr) {
-            if (rr < valid_rows) {
-                const uint8_t* vrow = vpg + vh * 2048 + rr * 128;
-                const int chunk16 = vbyte >> 4;
-                const uint8_t* src = vrow + (((chunk16 ^ (rr & 7)) << 4) | (vbyte & 15));
-                float vv[kDimsPerLane];
-                if (kDimsPerLane == 4) {
-                    const uint2 u = *reinterpret_cast<const uint2*>(src);
-                    vv[0] = bf_lo(u.x);
-                    vv[1] = bf_hi(u.x);
-                    vv[2] = bf_lo(u.y);
-                    vv[3] = bf_hi(u.y);
-                } else {
-                    const uint32_t u = *reinterpret_cast<const uint32_t*>(src);
-                    vv[0] = bf_lo(u);
-                    vv[1] = bf_hi(u);
-                }
-#pragma unroll
-                for (int j = 0; j < kMaxGroup; ++j) {
-                    if (j < g) {
-                        const float pj = s.pbuf[warp][j][rr];
-#pragma unroll
-                        for (int e = 0; e < kDimsPerLane; ++e) acc[j][e] = fmaf(pj, vv[e], acc[j][e]);
-                    }
-                }
-            }
-        }
-        __syncwarp();
-    }
-    // ---- merge the 4 warps (shared memory) ----
-    __syncwarp();
-    float* o_mine = s.o(warp);
-#pragma unroll
-    for (int j = 0; j < kMaxGroup; ++j) {
-        if (j < g) {
-            float lsum = l_lane[j];
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
-            if (lane == 0) {
-                s.m[warp][j] = m_run[j];
-                s.l[warp][j] = lsum;
-            }
-#pragma unroll
-            for (int e = 0; e < kDimsPerLane; ++e) o_mine[j * D + lane * kDimsPerLane + e] = acc[j][e];
-        }
-    }
-    __syncthreads();
-    __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) +
-                         (static_cast<size_t>(sp.query_start) * p.n_head + static_cast<size_t>(w.kvh) * g) * D;
-    const bool split = w.n_parts > 1;
-    for (int e = threadIdx.x; e < g * D; e += blockDim.x) {
-        const int j = e / D, d = e % D;
-        float M = -CUDART_INF_F;
-#pragma unroll
-        for (int q = 0; q < kDecWarps; ++q) M = fmaxf(M, s.m[q][j]);
-        float L = 0.f, O = 0.f;
-#pragma unroll
-        for (int q = 0; q < kDecWarps; ++q) {
-            const float f = ex2(s.m[q][j] - M);
-            L += f * s.l[q][j];
-            O += f * s.o(q)[j * D + d];
-        }
-        if (!split) {
-            out[static_cast<size_t>(j) * D + d] = __float2bfloat16_rn(O / L);
-        } else {
-            const int part = w.part_base + w.part_idx;
-            p.part_o[(static_cast<size_t>(part) * g + j) * D + d] = O;
-            if (d == 0) {
-                p.part_ml[(static_cast<size_t>(part) * g + j) * 2 + 0] = M;
-                p.part_ml[(static_cast<size_t>(part) * g + j) * 2 + 1] = L;
-            }
-        }
-    }
-    if (!split) return;
-    // ---- split-KV merge by the last-arriving part (same launch) ----
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        const int prev = atomicAdd(&p.counters[w.group], 1);
-        s.last = (prev == w.n_parts - 1);
-    }
-    __syncthreads();
-    if (!s.last) return;
-    __threadfence();
-    for (int e = threadIdx.x; e < g * D; e += blockDim.x) {
-        const int j = e / D, d = e % D;
-        float M = -CUDART_INF_F;
-        for (int q = 0; q < w.n_parts; ++q)
-            M = fmaxf(M, __ldcg(&p.part_ml[(static_cast<size_t>(w.part_base + q) * g + j) * 2]));
-        float L = 0.f, O = 0.f;
-        for (int q = 0; q < w.n_parts; ++q) {
-            const size_t b = static_cast<size_t>(w.part_base + q) * g + j;
-            const float f = ex2(__ldcg(&p.part_ml[b * 2]) - M);
-            L += f * __ldcg(&p.part_ml[b * 2 + 1]);
-            O += f * __ldcg(&p.part_o[b * D + d]);
-        }
-        out[static_cast<size_t>(j) * D + d] = __float2bfloat16_rn(O / L);
-    }
-    if (threadIdx.x == 0) p.counters[w.group] = 0; // self-reset for the next launch
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
 }
 
 template <int D, int G>
+__global__ void __launch_bounds__(dec_warps(G) * 32, 1)
+    attn_decode_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
+                       const AttnParams p) {
+    constexpr int KH = D / 64;
+    constexpr int kChunks = D / 16;       // 16 B chunks per lane and row (D/2 dims)
+    constexpr int kDimsPerLane = D / 32;
+    constexpr int kWarps = dec_warps(G);
+    constexpr int kFifo = kDecStages + 1;
+    using W = DecWarp<D, G>;
+    extern __shared__ uint8_t smem_raw[];
+    // align with pointer arithmetic on the __shared__ array so accesses stay LDS/STS
+    uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    const int warp = threadIdx.x >> 5;
+    const int lane = threadIdx.x & 31;
+    W& s = *reinterpret_cast<W*>(base + warp * sizeof(W));
+    const int g = p.group;
+    const float sl2 = p.scale_log2;
+    const uint32_t q_bytes = static_cast<uint32_t>(g * D * 2);
+    const uint32_t page_tx = 2u * KH * 16u * 128u;
+    int* queue = p.work_counter; // [0] next unit, [1] retired warps
+
+    if (lane == 0) {
+        for (int st = 0; st < kDecStages; ++st) {
+            mbar_init(&s.full[st], 1);
+            mbar_init(&s.qfull[st], 1);
+        }
+        mbar_fence_init();
+    }
+    __syncwarp();
+
+    // ---- unit FIFO: fetched in order; the issue and consume cursors walk the same sequence ----
+    int fifo[kFifo];
+    int n_fetched = 0;
+    bool exhausted = false;
+    auto fetch = [&]() {
+        int u = 0;
+        if (lane == 0) u = atomicAdd(&queue[0], 1);
+        u = __shfl_sync(0xffffffffu, u, 0);
+        if (u >= p.n_items) {
+            exhausted = true;
+            return;
+        }
+        fifo[n_fetched % kFifo] = u;
+        ++n_fetched;
+    };
+
+    int iss_unit = 0, iss_page = 0; // issue cursor
+    int issued = 0, consumed = 0;   // pages
+    // issue-side cache of the unit being issued: no global loads per page (the block-table
+    // slice of the unit, <= 64 pages, lives in two registers per lane)
+    int iss_np = -1, iss_kvh = 0, tbl_lo = 0, tbl_hi = 0;
+    const __nv_bfloat16* iss_q = nullptr;
+    fetch();
+    auto issue_one = [&]() -> bool {
+        while (true) {
+            if (iss_unit >= n_fetched) {
+                if (exhausted) return false;
+                fetch();
+                if (iss_unit >= n_fetched) return false;
+            }
+            if (iss_np < 0) { // first page of a new unit: load its descriptor once
+                const WorkItem wi = p.items[fifo[iss_unit % kFifo]];
+                const SpanDev sp = p.spans[wi.span];
+                iss_np = (wi.kv_end - wi.kv_begin + 15) >> 4;
+                iss_kvh = wi.kvh;
+                const int32_t* t = p.block_tables + sp.bt_off + (wi.kv_begin >> 4);
+                tbl_lo = lane < iss_np ? t[lane] : 0;
+                tbl_hi = lane + 32 < iss_np ? t[lane + 32] : 0;
+                iss_q = static_cast<const __nv_bfloat16*>(p.q) +
+                        (static_cast<size_t>(sp.query_start) * p.n_head + static_cast<size_t>(wi.kvh) * g) * D;
+            }
+            if (iss_page < iss_np) break;
+            ++iss_unit;
+            iss_page = 0;
+            iss_np = -1;
+        }
+        const int stage = issued % kDecStages;
+        int slot = __shfl_sync(0xffffffffu, iss_page < 32 ? tbl_lo : tbl_hi, iss_page & 31);
+        if (iss_page >= 64) { // unsplit long unit (PB_PLAN_NO_SPLIT): past the cached slice
+            const WorkItem wi = p.items[fifo[iss_unit % kFifo]];
+            slot = p.block_tables[p.spans[wi.span].bt_off + (wi.kv_begin >> 4) + iss_page];
+        }
+        if (lane == 0) {
+            fence_proxy_async_smem();
+            if (iss_page == 0) {
+                uint64_t* qb = &s.qfull[iss_unit % kDecStages];
+                mbar_arrive_expect_tx(qb, q_bytes);
+                bulk_g2s(s.qraw[iss_unit % kDecStages], iss_q, q_bytes, qb);
+            }
+            const int row = slot * 16;
+            uint8_t* dst = s.page[stage][0];
+            mbar_arrive_expect_tx(&s.full[stage], page_tx);
+            for (int h = 0; h < KH; ++h) {
+                tma_load_3d(dst + h * 2048, &tm_k, &s.full[stage], h * 64, iss_kvh, row);
+                tma_load_3d(dst + W::kPageBytes + h * 2048, &tm_v, &s.full[stage], h * 64, iss_kvh, row);
+            }
+        }
+        ++iss_page;
+        ++issued;
+        return true;
+    };
+    for (int i = 0; i < kDecStages; ++i)
+        if (!issue_one()) break;
+
+    const int r = lane & 15;   // page row scored by this lane
+    const int hh = lane >> 4;  // half of the dims
+    int con_unit = 0;
+    while (consumed < issued) {
+        // ---------------- start of a unit ----------------
+        const WorkItem w = p.items[fifo[con_unit % kFifo]];
+        const SpanDev sp = p.spans[w.span];
+        const int np = (w.kv_end - w.kv_begin + 15) >> 4;
+        mbar_wait(&s.qfull[con_unit % kDecStages], (con_unit / kDecStages) & 1);
+        {
+            const uint32_t* qr = reinterpret_cast<const uint32_t*>(s.qraw[con_unit % kDecStages]);
+            for (int e = lane; e < g * D / 2; e += 32) {
+                const uint32_t x = qr[e];
+                s.q[(2 * e) / D][(2 * e) % D] = bf_lo(x);
+                s.q[(2 * e) / D][(2 * e) % D + 1] = bf_hi(x);
+            }
+        }
+        __syncwarp();
+        float m_run[G], l_lane[G], acc[G][kDimsPerLane];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            m_run[j] = -CUDART_INF_F;
+            l_lane[j] = 0.f;
+#pragma unroll
+            for (int e = 0; e < kDimsPerLane; ++e) acc[j][e] = 0.f;
+        }
+        for (int pg = 0; pg < np; ++pg) {
+            const int stage = consumed % kDecStages;
+            mbar_wait(&s.full[stage], (consumed / kDecStages) & 1);
+            const uint8_t* kpg = s.page[stage][0];
+            const uint8_t* vpg = s.page[stage][1];
+            const int valid_rows = min(16, w.kv_end - (w.kv_begin + pg * 16));
+            // ---- scores: lane (r, hh) dots its row's half with every query head ----
+            float sc[G], sc2[G];
+#pragma unroll
+            for (int j = 0; j < G; ++j) sc[j] = sc2[j] = 0.f;
+#pragma unroll
+            for (int c = 0; c < kChunks; ++c) {
+                const int half = (D == 128) ? hh : 0;
+                const int cin = (D == 128) ? c : hh * kChunks + c;
+                const uint4 kv4 = *reinterpret_cast<const uint4*>(kpg + half * 2048 + r * 128 + ((cin ^ (r & 7)) << 4));
+                const float k8[8] = {bf_lo(kv4.x), bf_hi(kv4.x), bf_lo(kv4.y), bf_hi(kv4.y),
+                                     bf_lo(kv4.z), bf_hi(kv4.z), bf_lo(kv4.w), bf_hi(kv4.w)};
+                const int d0 = hh * (D / 2) + c * 8;
+#pragma unroll
+                for (int j = 0; j < G; ++j) {
+                    if (j < g) {
+                        const float4 qa = *reinterpret_cast<const float4*>(&s.q[j][d0]);
+                        const float4 qb = *reinterpret_cast<const float4*>(&s.q[j][d0 + 4]);
+                        float t = sc[j], v = sc2[j];
+                        t = fmaf(qa.x, k8[0], t);
+                        v = fmaf(qa.y, k8[1], v);
+                        t = fmaf(qa.z, k8[2], t);
+                        v = fmaf(qa.w, k8[3], v);
+                        t = fmaf(qb.x, k8[4], t);
+                        v = fmaf(qb.y, k8[5], v);
+                        t = fmaf(qb.z, k8[6], t);
+                        v = fmaf(qb.w, k8[7], v);
+                        sc[j] = t;
+                        sc2[j] = v;
+                    }
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < G; ++j) {
+                if (j < g) {
+                    float x = sc[j] + sc2[j];
+                    x += __shfl_xor_sync(0xffffffffu, x, 16);
+                    x = r < valid_rows ? x * sl2 : -CUDART_INF_F;
+                    float mx = x;
+                    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 1));
+                    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 2));
+                    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 4));
+                    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, 8));
+                    const float m_new = fmaxf(m_run[j], mx);
+                    const float corr = ex2(m_run[j] - m_new);
+                    const float pr = ex2(x - m_new);
+                    m_run[j] = m_new;
+                    l_lane[j] = l_lane[j] * corr + (hh == 0 ? pr : 0.f);
+#pragma unroll
+                    for (int e = 0; e < kDimsPerLane; ++e) acc[j][e] *= corr;
+                    if (hh == 0) s.pbuf[j][r] = pr;
+                }
+            }
+            __syncwarp();
+            // ---- PV: lane owns dims [lane*kDimsPerLane, +kDimsPerLane) ----
+            const int vh = (D == 128) ? (lane >> 4) : 0;
+            const int vbyte = (D == 128) ? ((lane & 15) * 8) : (lane * 4);
+#pragma unroll
+            for (int rr = 0; rr < 16; ++rr) {
+                if (rr < valid_rows) {
+                    const uint8_t* src = vpg + vh * 2048 + rr * 128 + ((((vbyte >> 4) ^ (rr & 7)) << 4) | (vbyte & 15));
+                    float vv[kDimsPerLane];
+                    if constexpr (kDimsPerLane == 4) {
+                        const uint2 uv = *reinterpret_cast<const uint2*>(src);
+                        vv[0] = bf_lo(uv.x);
+                        vv[1] = bf_hi(uv.x);
+                        vv[2] = bf_lo(uv.y);
+                        vv[3] = bf_hi(uv.y);
+                    } else {
+                        const uint32_t uv = *reinterpret_cast<const uint32_t*>(src);
+                        vv[0] = bf_lo(uv);
+                        vv[1] = bf_hi(uv);
+                    }
+#pragma unroll
+                    for (int j = 0; j < G; ++j) {
+                        if (j < g) {
+                            const float pj = s.pbuf[j][rr];
+#pragma unroll
+                            for (int e = 0; e < kDimsPerLane; ++e) acc[j][e] = fmaf(pj, vv[e], acc[j][e]);
+                        }
+                    }
+                }
+            }
+            __syncwarp(); // stage and pbuf reads done before they are overwritten
+            ++consumed;
+            issue_one();
+        }
+        // ---------------- end of a unit: normalise or publish a split partial ----------------
+        float l_tot[G];
+#pragma unroll
+        for (int j = 0; j < G; ++j) {
+            float lsum = l_lane[j];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) lsum += __shfl_xor_sync(0xffffffffu, lsum, o);
+            l_tot[j] = lsum;
+        }
+        __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out) +
+                             (static_cast<size_t>(sp.query_start) * p.n_head + static_cast<size_t>(w.kvh) * g) * D;
+        const int d0 = lane * kDimsPerLane;
+        if (w.n_parts <= 1) {
+#pragma unroll
+            for (int j = 0; j < G; ++j)
+                if (j < g) {
+                    const float inv = 1.f / l_tot[j];
+#pragma unroll
+                    for (int e = 0; e < kDimsPerLane; ++e)
+                        out[static_cast<size_t>(j) * D + d0 + e] = __float2bfloat16_rn(acc[j][e] * inv);
+                }
+        } else {
+            const int part = w.part_base + w.part_idx;
+#pragma unroll
+            for (int j = 0; j < G; ++j)
+                if (j < g) {
+#pragma unroll
+                    for (int e = 0; e < kDimsPerLane; ++e)
+                        p.part_o[(static_cast<size_t>(part) * g + j) * D + d0 + e] = acc[j][e];
+                    if (lane == 0) {
+                        p.part_ml[(static_cast<size_t>(part) * g + j) * 2 + 0] = m_run[j];
+                        p.part_ml[(static_cast<size_t>(part) * g + j) * 2 + 1] = l_tot[j];
+                    }
+                }
+            __threadfence();
+            __syncwarp();
+            int last = 0;
+            if (lane == 0) last = atomicAdd(&p.counters[w.group], 1) == w.n_parts - 1;
+            last = __shfl_sync(0xffffffffu, last, 0);
+            if (last) {
+                __threadfence();
+#pragma unroll
+                for (int j = 0; j < G; ++j)
+                    if (j < g) {
+                        float M = -CUDART_INF_F;
+                        for (int q = 0; q < w.n_parts; ++q)
+                            M = fmaxf(M, __ldcg(&p.part_ml[(static_cast<size_t>(w.part_base + q) * g + j) * 2]));
+                        float L = 0.f, O[kDimsPerLane];
+#pragma unroll
+                        for (int e = 0; e < kDimsPerLane; ++e) O[e] = 0.f;
+                        for (int q = 0; q < w.n_parts; ++q) {
+                            const size_t b = static_cast<size_t>(w.part_base + q) * g + j;
+                            const float f = ex2(__ldcg(&p.part_ml[b * 2]) - M);
+                            L += f * __ldcg(&p.part_ml[b * 2 + 1]);
+#pragma unroll
+                            for (int e = 0; e < kDimsPerLane; ++e) O[e] += f * __ldcg(&p.part_o[b * D + d0 + e]);
+                        }
+                        const float inv = 1.f / L;
+#pragma unroll
+                        for (int e = 0; e < kDimsPerLane; ++e)
+                            out[static_cast<size_t>(j) * D + d0 + e] = __float2bfloat16_rn(O[e] * inv);
+                    }
+                if (lane == 0) p.counters[w.group] = 0; // self-reset for the next launch
+            }
+        }
+        ++con_unit;
+    }
+    // retire: the last warp of the launch resets the queue for the next launch
+    if (lane == 0) {
+        const int total = static_cast<int>(gridDim.x) * kWarps;
+        if (atomicAdd(&queue[1], 1) == total - 1) {
+            queue[0] = 0;
+            queue[1] = 0;
+            __threadfence();
+        }
+    }
+}
+
+int g_dec_sms = 0;
+
+template <int D, int G>
 void launch_decode_t(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st) {
-    const size_t smem = sizeof(DecSmem<D, G>) + 1024;
+    const size_t smem = sizeof(DecWarp<D, G>) * dec_warps(G) + 1024;
     static bool attr = false;
     if (!attr) {
         cuda_check(cudaFuncSetAttribute(attn_decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -294,7 +375,13 @@ void launch_decode_t(const AttnParams& p, const CUtensorMap* maps, cudaStream_t 
                    "cudaFuncSetAttribute(decode smem)");
         attr = true;
     }
-    attn_decode_kernel<D, G><<<p.n_items, kDecWarps * 32, smem, st>>>(maps[1], maps[2], p);
+    if (g_dec_sms == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_dec_sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const int grid = std::max(1, std::min(g_dec_sms, (p.n_items + dec_warps(G) - 1) / dec_warps(G)));
+    attn_decode_kernel<D, G><<<grid, dec_warps(G) * 32, smem, st>>>(maps[1], maps[2], p);
     cuda_check(cudaGetLastError(), "attn_decode launch");
     count_launch();
 }

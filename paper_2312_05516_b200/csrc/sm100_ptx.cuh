@@ -164,15 +164,17 @@ __device__ __forceinline__ float ex2(float x) {
 
 // 2^x on the FMA/ALU pipes (for x <= ~8): round-to-nearest integer j via the 1.5*2^23
 // magic add, cubic fit of 2^f on [-0.5, 0.5] (max rel. err 1.8e-4, far below bf16's 3.9e-3),
-// exponent added as integer bits.  x = -inf / very negative clamps to ~2^-127 (denormal ~0).
+// exponent added as integer bits.  x < -126 (incl. masked -inf) returns exactly 0; the
+// clamp keeps the integer exponent add from wrapping into the sign bit.
 __device__ __forceinline__ float exp2_poly3(float x) {
-    x = fmaxf(x, -127.f);
-    const float r = x + 12582912.f;
-    const float f = x - (r - 12582912.f);
+    const float xc = fmaxf(x, -126.f);
+    const float r = xc + 12582912.f;
+    const float f = xc - (r - 12582912.f);
     float p = fmaf(0.05324155f, f, 0.24228422f);
     p = fmaf(p, f, 0.69354963f);
     p = fmaf(p, f, 0.9999545f);
-    return __int_as_float(__float_as_int(p) + (__float_as_int(r) << 23));
+    const float y = __int_as_float(__float_as_int(p) + (__float_as_int(r) << 23));
+    return x < -126.f ? 0.f : y;
 }
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
