@@ -170,6 +170,32 @@ pb_status pb_kv_append(const pb_attn_shape* shape, int32_t n_spans, const int64_
 pb_status pb_fill_splitmix_unit(void* dst, int32_t dtype, int64_t n, uint64_t seed,
                                 uint64_t first_draw, void* stream);
 
+/* ===================================================================== CPU-tier swap engine
+ * Pinned host tier [host_slot][layer][K|V][page] (one chunk = chunk_bytes contiguous,
+ * src/model_config.cpp:36-40) and the ordered, layer-pipelined copies the reference only
+ * models as a timeline (src/swap_engine.cpp:21-53):
+ *   1. swap-out GATHER of device pages on compute_stream first (device slots vacated by
+ *      swap-out may be refilled in the same step, src/paged_kv_cache.cpp:28-37);
+ *   2. swap-in per layer on copy_stream: batched H2D into staging, scatter kernel into the
+ *      pools, event per layer (pb_swap_wait_layer = "attention of layer l may start",
+ *      PAPER.md:617-619);
+ *   3. swap-out D2H after the swap-ins on copy_stream (schedule_swap_out_start, :50-53).
+ * Pools: k_pool / v_pool hold n_layer pools at layer_stride bytes apart, pages of
+ * page_bytes.  Moves come from pb_cache_apply_evictions (device src -> host dst) and
+ * pb_cache_restore (host src -> device dst). */
+typedef struct pb_kv_tier pb_kv_tier;
+typedef struct pb_slot_move pb_slot_move; /* defined with the bookkeeping API below */
+pb_status pb_tier_create(int32_t n_layer, int32_t host_slots, int64_t page_bytes,
+                         int32_t max_chunks_per_step, pb_kv_tier** out);
+void pb_tier_destroy(pb_kv_tier* tier);
+void* pb_tier_host_base(pb_kv_tier* tier);
+int64_t pb_tier_chunk_bytes(const pb_kv_tier* tier);
+pb_status pb_swap_step(pb_kv_tier* tier, void* k_pool, void* v_pool, int64_t layer_stride,
+                       const pb_slot_move* out_moves, int64_t n_out, const pb_slot_move* in_moves,
+                       int64_t n_in, void* compute_stream, void* copy_stream);
+pb_status pb_swap_wait_layer(pb_kv_tier* tier, int32_t layer, void* compute_stream);
+pb_status pb_swap_sync(pb_kv_tier* tier);
+
 /* ===================================================================== KV page bookkeeping
  * Two-tier slot allocator + per-conversation chunk index with the exact slot semantics of
  * kvsim::PagedKvCache (include/kvsim/paged_kv_cache.hpp:52-153, src/paged_kv_cache.cpp):

@@ -433,3 +433,65 @@ class KvCache:
         buf = ctypes.create_string_buffer(int(n) + 1)
         lib.pb_cache_dump(self._h, buf, n + 1)
         return buf.value.decode()
+
+
+# ============================================================================ swap engine
+_TIER_SIGS = {
+    "pb_tier_create": (_I32, [_I32, _I32, _I64, _I32, ctypes.POINTER(_P)]),
+    "pb_tier_destroy": (None, [_P]),
+    "pb_tier_host_base": (_P, [_P]),
+    "pb_tier_chunk_bytes": (_I64, [_P]),
+    "pb_swap_step": (_I32, [_P, _P, _P, _I64, _P, _I64, _P, _I64, _P, _P]),
+    "pb_swap_wait_layer": (_I32, [_P, _I32, _P]),
+    "pb_swap_sync": (_I32, [_P]),
+}
+for _name, (_res, _args) in _TIER_SIGS.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+_SIGS.update(_TIER_SIGS)
+
+
+def _moves_array(moves):
+    arr = (SlotMove * max(1, len(moves)))()
+    for i, (c, s, d) in enumerate(moves):
+        arr[i].chunk, arr[i].src_slot, arr[i].dst_slot = c, s, d
+    return arr
+
+
+class KvTier:
+    """pb_kv_tier: pinned host tier + ordered, layer-pipelined swap copies."""
+
+    def __init__(self, n_layer: int, host_slots: int, page_bytes: int, max_chunks_per_step: int):
+        h = _P()
+        check(lib.pb_tier_create(n_layer, host_slots, page_bytes, max_chunks_per_step, ctypes.byref(h)))
+        self._h = h
+        self.n_layer, self.host_slots, self.page_bytes = n_layer, host_slots, page_bytes
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.pb_tier_destroy(h)
+            self._h = None
+
+    @property
+    def chunk_bytes(self) -> int:
+        return int(lib.pb_tier_chunk_bytes(self._h))
+
+    def host_view(self) -> np.ndarray:
+        """The pinned host tier as a numpy byte array [host_slot][layer][K|V][page]."""
+        base = lib.pb_tier_host_base(self._h)
+        buf = (ctypes.c_uint8 * (self.host_slots * self.chunk_bytes)).from_address(base)
+        return np.frombuffer(buf, dtype=np.uint8)
+
+    def step(self, k_pool: int, v_pool: int, layer_stride: int, out_moves, in_moves,
+             compute_stream: Optional[int] = None, copy_stream: Optional[int] = None) -> None:
+        om, im = _moves_array(out_moves), _moves_array(in_moves)
+        check(lib.pb_swap_step(self._h, k_pool, v_pool, layer_stride, om, len(out_moves), im, len(in_moves),
+                               compute_stream, copy_stream))
+
+    def wait_layer(self, layer: int, compute_stream: Optional[int] = None) -> None:
+        check(lib.pb_swap_wait_layer(self._h, layer, compute_stream))
+
+    def sync(self) -> None:
+        check(lib.pb_swap_sync(self._h))

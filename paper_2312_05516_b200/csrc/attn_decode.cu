@@ -37,15 +37,26 @@ using namespace pb::sm100;
 constexpr int kDecStages = 3;
 constexpr int kMaxGroup = 16;
 
-__host__ __device__ constexpr int dec_warps(int G) { return G <= 8 ? 6 : 4; }
+// warps per CTA (one CTA per SM): as many independent page streams as shared memory allows
+__host__ __device__ constexpr int dec_warps(int G) { return G <= 4 ? 7 : (G <= 8 ? 6 : 4); }
+
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { // FFMA2 (sm_100)
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;"
+        : "=l"(d)
+        : "l"(*reinterpret_cast<uint64_t*>(&a)), "l"(*reinterpret_cast<uint64_t*>(&b)),
+          "l"(*reinterpret_cast<uint64_t*>(&c)));
+    return *reinterpret_cast<float2*>(&d);
+}
 
 template <int D, int G>
 struct __align__(1024) DecWarp {
     static constexpr int KH = D / 64;
     static constexpr int kPageBytes = 16 * D * 2;        // one kv head, 16 rows
     uint8_t page[kDecStages][2][kPageBytes];             // [stage][K|V][half][row][128 B]
-    uint8_t qraw[kDecStages][G * D * 2];                 // bf16 q rows, slot = unit seq % stages
-    float q[G][D];                                       // fp32 q of the unit being consumed
+    // q rows of a unit, slot = unit seq % stages: bf16 by cp.async.bulk, widened to fp32 in
+    // place when the unit starts
+    uint8_t qraw[kDecStages][G * D * 4];
     float pbuf[G][16];                                   // page probabilities
     uint64_t full[kDecStages];
     uint64_t qfull[kDecStages];
@@ -176,22 +187,28 @@ __global__ void __launch_bounds__(dec_warps(G) * 32, 1)
         const SpanDev sp = p.spans[w.span];
         const int np = (w.kv_end - w.kv_begin + 15) >> 4;
         mbar_wait(&s.qfull[con_unit % kDecStages], (con_unit / kDecStages) & 1);
+        float* qf = reinterpret_cast<float*>(s.qraw[con_unit % kDecStages]); // [g][D] fp32 after widening
         {
-            const uint32_t* qr = reinterpret_cast<const uint32_t*>(s.qraw[con_unit % kDecStages]);
-            for (int e = lane; e < g * D / 2; e += 32) {
-                const uint32_t x = qr[e];
-                s.q[(2 * e) / D][(2 * e) % D] = bf_lo(x);
-                s.q[(2 * e) / D][(2 * e) % D + 1] = bf_hi(x);
-            }
+            constexpr int kWords = G * D / 2 / 32; // bf16 pairs per lane (upper bound)
+            uint32_t wv[kWords];
+            const uint32_t* qr = reinterpret_cast<const uint32_t*>(qf);
+#pragma unroll
+            for (int k = 0; k < kWords; ++k) wv[k] = (lane + 32 * k < g * D / 2) ? qr[lane + 32 * k] : 0u;
+            __syncwarp();
+#pragma unroll
+            for (int k = 0; k < kWords; ++k)
+                if (lane + 32 * k < g * D / 2)
+                    reinterpret_cast<float2*>(qf)[lane + 32 * k] = make_float2(bf_lo(wv[k]), bf_hi(wv[k]));
         }
         __syncwarp();
-        float m_run[G], l_lane[G], acc[G][kDimsPerLane];
+        float m_run[G], l_lane[G];
+        float2 acc[G][kDimsPerLane / 2]; // FFMA2 pairs of this lane's output dims
 #pragma unroll
         for (int j = 0; j < G; ++j) {
             m_run[j] = -CUDART_INF_F;
             l_lane[j] = 0.f;
 #pragma unroll
-            for (int e = 0; e < kDimsPerLane; ++e) acc[j][e] = 0.f;
+            for (int e = 0; e < kDimsPerLane / 2; ++e) acc[j][e] = make_float2(0.f, 0.f);
         }
         for (int pg = 0; pg < np; ++pg) {
             const int stage = consumed % kDecStages;
@@ -200,40 +217,35 @@ __global__ void __launch_bounds__(dec_warps(G) * 32, 1)
             const uint8_t* vpg = s.page[stage][1];
             const int valid_rows = min(16, w.kv_end - (w.kv_begin + pg * 16));
             // ---- scores: lane (r, hh) dots its row's half with every query head ----
-            float sc[G], sc2[G];
+            float2 sc[G]; // two partial sums per head (FFMA2 lanes)
 #pragma unroll
-            for (int j = 0; j < G; ++j) sc[j] = sc2[j] = 0.f;
+            for (int j = 0; j < G; ++j) sc[j] = make_float2(0.f, 0.f);
 #pragma unroll
             for (int c = 0; c < kChunks; ++c) {
                 const int half = (D == 128) ? hh : 0;
                 const int cin = (D == 128) ? c : hh * kChunks + c;
                 const uint4 kv4 = *reinterpret_cast<const uint4*>(kpg + half * 2048 + r * 128 + ((cin ^ (r & 7)) << 4));
-                const float k8[8] = {bf_lo(kv4.x), bf_hi(kv4.x), bf_lo(kv4.y), bf_hi(kv4.y),
-                                     bf_lo(kv4.z), bf_hi(kv4.z), bf_lo(kv4.w), bf_hi(kv4.w)};
+                const float2 k2[4] = {make_float2(bf_lo(kv4.x), bf_hi(kv4.x)), make_float2(bf_lo(kv4.y), bf_hi(kv4.y)),
+                                      make_float2(bf_lo(kv4.z), bf_hi(kv4.z)), make_float2(bf_lo(kv4.w), bf_hi(kv4.w))};
                 const int d0 = hh * (D / 2) + c * 8;
 #pragma unroll
                 for (int j = 0; j < G; ++j) {
                     if (j < g) {
-                        const float4 qa = *reinterpret_cast<const float4*>(&s.q[j][d0]);
-                        const float4 qb = *reinterpret_cast<const float4*>(&s.q[j][d0 + 4]);
-                        float t = sc[j], v = sc2[j];
-                        t = fmaf(qa.x, k8[0], t);
-                        v = fmaf(qa.y, k8[1], v);
-                        t = fmaf(qa.z, k8[2], t);
-                        v = fmaf(qa.w, k8[3], v);
-                        t = fmaf(qb.x, k8[4], t);
-                        v = fmaf(qb.y, k8[5], v);
-                        t = fmaf(qb.z, k8[6], t);
-                        v = fmaf(qb.w, k8[7], v);
+                        const float4 qa = *reinterpret_cast<const float4*>(qf + j * D + d0);
+                        const float4 qb = *reinterpret_cast<const float4*>(qf + j * D + d0 + 4);
+                        float2 t = sc[j];
+                        t = ffma2(make_float2(qa.x, qa.y), k2[0], t);
+                        t = ffma2(make_float2(qa.z, qa.w), k2[1], t);
+                        t = ffma2(make_float2(qb.x, qb.y), k2[2], t);
+                        t = ffma2(make_float2(qb.z, qb.w), k2[3], t);
                         sc[j] = t;
-                        sc2[j] = v;
                     }
                 }
             }
 #pragma unroll
             for (int j = 0; j < G; ++j) {
                 if (j < g) {
-                    float x = sc[j] + sc2[j];
+                    float x = sc[j].x + sc[j].y;
                     x += __shfl_xor_sync(0xffffffffu, x, 16);
                     x = r < valid_rows ? x * sl2 : -CUDART_INF_F;
                     float mx = x;
@@ -247,7 +259,7 @@ __global__ void __launch_bounds__(dec_warps(G) * 32, 1)
                     m_run[j] = m_new;
                     l_lane[j] = l_lane[j] * corr + (hh == 0 ? pr : 0.f);
 #pragma unroll
-                    for (int e = 0; e < kDimsPerLane; ++e) acc[j][e] *= corr;
+                    for (int e = 0; e < kDimsPerLane / 2; ++e) acc[j][e] = make_float2(acc[j][e].x * corr, acc[j][e].y * corr);
                     if (hh == 0) s.pbuf[j][r] = pr;
                 }
             }
@@ -259,24 +271,21 @@ __global__ void __launch_bounds__(dec_warps(G) * 32, 1)
             for (int rr = 0; rr < 16; ++rr) {
                 if (rr < valid_rows) {
                     const uint8_t* src = vpg + vh * 2048 + rr * 128 + ((((vbyte >> 4) ^ (rr & 7)) << 4) | (vbyte & 15));
-                    float vv[kDimsPerLane];
+                    float2 vv[kDimsPerLane / 2];
                     if constexpr (kDimsPerLane == 4) {
                         const uint2 uv = *reinterpret_cast<const uint2*>(src);
-                        vv[0] = bf_lo(uv.x);
-                        vv[1] = bf_hi(uv.x);
-                        vv[2] = bf_lo(uv.y);
-                        vv[3] = bf_hi(uv.y);
+                        vv[0] = make_float2(bf_lo(uv.x), bf_hi(uv.x));
+                        vv[1] = make_float2(bf_lo(uv.y), bf_hi(uv.y));
                     } else {
                         const uint32_t uv = *reinterpret_cast<const uint32_t*>(src);
-                        vv[0] = bf_lo(uv);
-                        vv[1] = bf_hi(uv);
+                        vv[0] = make_float2(bf_lo(uv), bf_hi(uv));
                     }
 #pragma unroll
                     for (int j = 0; j < G; ++j) {
                         if (j < g) {
                             const float pj = s.pbuf[j][rr];
 #pragma unroll
-                            for (int e = 0; e < kDimsPerLane; ++e) acc[j][e] = fmaf(pj, vv[e], acc[j][e]);
+                            for (int e = 0; e < kDimsPerLane / 2; ++e) acc[j][e] = ffma2(make_float2(pj, pj), vv[e], acc[j][e]);
                         }
                     }
                 }
@@ -303,8 +312,10 @@ __global__ void __launch_bounds__(dec_warps(G) * 32, 1)
                 if (j < g) {
                     const float inv = 1.f / l_tot[j];
 #pragma unroll
-                    for (int e = 0; e < kDimsPerLane; ++e)
-                        out[static_cast<size_t>(j) * D + d0 + e] = __float2bfloat16_rn(acc[j][e] * inv);
+                    for (int e = 0; e < kDimsPerLane / 2; ++e) {
+                        out[static_cast<size_t>(j) * D + d0 + 2 * e] = __float2bfloat16_rn(acc[j][e].x * inv);
+                        out[static_cast<size_t>(j) * D + d0 + 2 * e + 1] = __float2bfloat16_rn(acc[j][e].y * inv);
+                    }
                 }
         } else {
             const int part = w.part_base + w.part_idx;
@@ -312,8 +323,10 @@ __global__ void __launch_bounds__(dec_warps(G) * 32, 1)
             for (int j = 0; j < G; ++j)
                 if (j < g) {
 #pragma unroll
-                    for (int e = 0; e < kDimsPerLane; ++e)
-                        p.part_o[(static_cast<size_t>(part) * g + j) * D + d0 + e] = acc[j][e];
+                    for (int e = 0; e < kDimsPerLane / 2; ++e) {
+                        p.part_o[(static_cast<size_t>(part) * g + j) * D + d0 + 2 * e] = acc[j][e].x;
+                        p.part_o[(static_cast<size_t>(part) * g + j) * D + d0 + 2 * e + 1] = acc[j][e].y;
+                    }
                     if (lane == 0) {
                         p.part_ml[(static_cast<size_t>(part) * g + j) * 2 + 0] = m_run[j];
                         p.part_ml[(static_cast<size_t>(part) * g + j) * 2 + 1] = l_tot[j];

@@ -1,0 +1,252 @@
+// CPU-tier swap engine: moves KV pages between the HBM page pools and a pinned host tier,
+// layer-pipelined and ordered the way the reference's timeline model prescribes
+// (/root/reference/proj/src/swap_engine.cpp:21-53):
+//   * swap-in is issued layer by layer (layer l of every chunk before layer l+1); an event per
+//     layer lets the compute stream start layer l's attention as soon as its pages landed
+//     (the LayerDependencyAuditor rule of src/event_log.cpp:90-118);
+//   * swap-out (D2H) is queued behind the step's swap-ins on the copy stream, so the two
+//     directions never contend (schedule_swap_out_start, :50-53);
+//   * the swap-out GATHER (device pages -> contiguous staging) runs first, on the compute
+//     stream, so device slots vacated by swap-out can be refilled in the same step by restore /
+//     rematerialize / append (the reference reuses them LIFO, src/paged_kv_cache.cpp:28-37)
+//     without a read-after-write hazard; the swap-in scatter waits for that gather.
+// Host tier layout: [host_slot][layer][K|V][page] — one chunk's bytes for all layers are
+// contiguous (= ModelConfig::chunk_bytes per worker, src/model_config.cpp:36-40), so a
+// swap-out is one D2H per chunk; a swap-in reads one (K,V) block per chunk per layer.
+#include "pb_common.hpp"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <memory>
+#include <vector>
+
+namespace pb {
+namespace {
+
+__global__ void __launch_bounds__(256) swap_gather_kernel(const uint8_t* __restrict__ kpool,
+                                                          const uint8_t* __restrict__ vpool, int64_t layer_stride,
+                                                          int64_t page_bytes, const int32_t* __restrict__ slots,
+                                                          int32_t n, int32_t n_layer, uint8_t* __restrict__ stage) {
+    // job = (chunk i, layer l, K|V); staging[((i*L + l)*2 + kv) * page]
+    const int64_t jobs = static_cast<int64_t>(n) * n_layer * 2;
+    const int64_t vecs = page_bytes / 16;
+    for (int64_t job = blockIdx.x; job < jobs; job += gridDim.x) {
+        const int kv = static_cast<int>(job & 1);
+        const int64_t il = job >> 1;
+        const int64_t i = il / n_layer, l = il % n_layer;
+        const int4* src = reinterpret_cast<const int4*>((kv ? vpool : kpool) + l * layer_stride +
+                                                        static_cast<int64_t>(slots[i]) * page_bytes);
+        int4* dst = reinterpret_cast<int4*>(stage + job * page_bytes);
+        for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) __stcs(dst + v, __ldcs(src + v));
+    }
+}
+
+__global__ void __launch_bounds__(256) swap_scatter_layer_kernel(const uint8_t* __restrict__ stage,
+                                                                 uint8_t* __restrict__ kpool_l,
+                                                                 uint8_t* __restrict__ vpool_l, int64_t page_bytes,
+                                                                 const int32_t* __restrict__ slots, int32_t n) {
+    // staging for one layer: [chunk i][K|V][page]
+    const int64_t jobs = static_cast<int64_t>(n) * 2;
+    const int64_t vecs = page_bytes / 16;
+    for (int64_t job = blockIdx.x; job < jobs; job += gridDim.x) {
+        const int kv = static_cast<int>(job & 1);
+        const int64_t i = job >> 1;
+        const int4* src = reinterpret_cast<const int4*>(stage + job * page_bytes);
+        int4* dst = reinterpret_cast<int4*>((kv ? vpool_l : kpool_l) + static_cast<int64_t>(slots[i]) * page_bytes);
+        for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) __stcs(dst + v, __ldcs(src + v));
+    }
+}
+
+int n_sms() {
+    static int s = 0;
+    if (!s) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+        if (s <= 0) s = 148;
+    }
+    return s;
+}
+
+// Batched copies (one driver call per batch, cudaMemcpyBatchAsync); per-copy fallback if the
+// runtime refuses the batch.
+void copy_batch(std::vector<void*>& dst, std::vector<void*>& src, std::vector<size_t>& sizes, cudaStream_t st) {
+    if (dst.empty()) return;
+    cudaMemcpyAttributes attr{};
+    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+    size_t attr_idx = 0, fail_idx = 0;
+    cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), sizes.data(), dst.size(), &attr, &attr_idx, 1,
+                                         &fail_idx, st);
+    if (e == cudaSuccess) return;
+    cudaGetLastError();
+    for (size_t i = 0; i < dst.size(); ++i)
+        cuda_check(cudaMemcpyAsync(dst[i], src[i], sizes[i], cudaMemcpyDefault, st), "swap copy");
+}
+
+} // namespace
+} // namespace pb
+
+using namespace pb;
+
+struct pb_kv_tier {
+    int32_t n_layer = 0, host_slots = 0, max_chunks = 0;
+    int64_t page_bytes = 0;
+    uint8_t* host = nullptr;       // pinned [host_slot][layer][K|V][page]
+    uint8_t* stage_out = nullptr;  // device [chunk][layer][K|V][page]
+    uint8_t* stage_in = nullptr;   // device [layer][chunk][K|V][page]
+    int32_t* d_slots = nullptr;    // device: [out slots | in slots]
+    int32_t* h_slots = nullptr;    // pinned staging for the slot lists
+    cudaEvent_t gathered = nullptr, done = nullptr;
+    std::vector<cudaEvent_t> layer_ready;
+    bool any_in = false;
+    int64_t chunk_bytes() const { return static_cast<int64_t>(n_layer) * 2 * page_bytes; }
+};
+
+extern "C" {
+
+pb_status pb_tier_create(int32_t n_layer, int32_t host_slots, int64_t page_bytes, int32_t max_chunks_per_step,
+                         pb_kv_tier** out) {
+    return guarded([&] {
+        if (!out) fail(PB_ERR_ERROR, "null out");
+        *out = nullptr;
+        if (n_layer < 1 || host_slots < 0 || page_bytes <= 0 || page_bytes % 16 || max_chunks_per_step < 1)
+            fail(PB_ERR_CONFIG, "bad tier geometry (page_bytes must be a positive multiple of 16)");
+        auto T = std::make_unique<pb_kv_tier>();
+        T->n_layer = n_layer;
+        T->host_slots = host_slots;
+        T->page_bytes = page_bytes;
+        T->max_chunks = max_chunks_per_step;
+        const size_t host_bytes = static_cast<size_t>(std::max(1, host_slots)) * T->chunk_bytes();
+        if (cudaHostAlloc(reinterpret_cast<void**>(&T->host), host_bytes, cudaHostAllocPortable) != cudaSuccess) {
+            cudaGetLastError();
+            fail(PB_ERR_INSUFFICIENT_HOST_MEMORY, "pinned host tier allocation failed");
+        }
+        const size_t stage_bytes = static_cast<size_t>(max_chunks_per_step) * T->chunk_bytes();
+        if (cudaMalloc(&T->stage_out, stage_bytes) != cudaSuccess || cudaMalloc(&T->stage_in, stage_bytes) != cudaSuccess) {
+            cudaGetLastError();
+            fail(PB_ERR_INSUFFICIENT_DEVICE_MEMORY, "swap staging allocation failed");
+        }
+        cuda_check(cudaMalloc(&T->d_slots, sizeof(int32_t) * 2 * max_chunks_per_step), "cudaMalloc(slots)");
+        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&T->h_slots), sizeof(int32_t) * 2 * max_chunks_per_step,
+                                 cudaHostAllocPortable),
+                   "cudaHostAlloc(slots)");
+        cuda_check(cudaEventCreateWithFlags(&T->gathered, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventCreateWithFlags(&T->done, cudaEventDisableTiming), "event");
+        T->layer_ready.resize(static_cast<size_t>(n_layer));
+        for (auto& e : T->layer_ready) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+        *out = T.release();
+    });
+}
+
+void pb_tier_destroy(pb_kv_tier* T) {
+    if (!T) return;
+    if (T->done) cudaEventSynchronize(T->done);
+    cudaFreeHost(T->host);
+    cudaFree(T->stage_out);
+    cudaFree(T->stage_in);
+    cudaFree(T->d_slots);
+    cudaFreeHost(T->h_slots);
+    if (T->gathered) cudaEventDestroy(T->gathered);
+    if (T->done) cudaEventDestroy(T->done);
+    for (auto e : T->layer_ready) cudaEventDestroy(e);
+    delete T;
+}
+
+void* pb_tier_host_base(pb_kv_tier* T) { return T ? T->host : nullptr; }
+
+int64_t pb_tier_chunk_bytes(const pb_kv_tier* T) { return T ? T->chunk_bytes() : 0; }
+
+pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_stride, const pb_slot_move* out_moves,
+                       int64_t n_out, const pb_slot_move* in_moves, int64_t n_in, void* compute_stream,
+                       void* copy_stream) {
+    return guarded([&] {
+        if (!T) fail(PB_ERR_ERROR, "null tier");
+        if (n_out < 0 || n_in < 0 || n_out > T->max_chunks || n_in > T->max_chunks)
+            fail(PB_ERR_DIMENSION_MISMATCH, "swap batch exceeds the tier's max_chunks_per_step");
+        for (int64_t i = 0; i < n_out; ++i)
+            if (out_moves[i].src_slot < 0 || out_moves[i].dst_slot < 0 || out_moves[i].dst_slot >= T->host_slots)
+                fail(PB_ERR_ERROR, "swap-out move needs a device source and a host destination slot");
+        for (int64_t i = 0; i < n_in; ++i)
+            if (in_moves[i].src_slot < 0 || in_moves[i].src_slot >= T->host_slots || in_moves[i].dst_slot < 0)
+                fail(PB_ERR_ERROR, "swap-in move needs a host source and a device destination slot");
+        cudaStream_t cs = as_stream(compute_stream), xs = as_stream(copy_stream);
+        // the previous step's transfers must be done before the slot staging is rewritten
+        cuda_check(cudaEventSynchronize(T->done), "swap step ordering");
+        for (int64_t i = 0; i < n_out; ++i) T->h_slots[i] = out_moves[i].src_slot;
+        for (int64_t i = 0; i < n_in; ++i) T->h_slots[T->max_chunks + i] = in_moves[i].dst_slot;
+        cuda_check(cudaMemcpyAsync(T->d_slots, T->h_slots, sizeof(int32_t) * 2 * T->max_chunks,
+                                   cudaMemcpyHostToDevice, cs),
+                   "slot upload");
+        const int64_t pb = T->page_bytes;
+        auto* kp = static_cast<uint8_t*>(k_pool);
+        auto* vp = static_cast<uint8_t*>(v_pool);
+        // 1. swap-out gather on the compute stream, before any same-step write to those slots
+        if (n_out > 0) {
+            const int64_t jobs = n_out * T->n_layer * 2;
+            const int grid = static_cast<int>(std::min<int64_t>(jobs, n_sms() * 8));
+            swap_gather_kernel<<<grid, 256, 0, cs>>>(kp, vp, layer_stride, pb, T->d_slots, static_cast<int32_t>(n_out),
+                                                     T->n_layer, T->stage_out);
+            cuda_check(cudaGetLastError(), "swap gather");
+            count_launch();
+        }
+        cuda_check(cudaEventRecord(T->gathered, cs), "event record");
+        cuda_check(cudaStreamWaitEvent(xs, T->gathered, 0), "stream wait");
+        // 2. swap-in, layer by layer: H2D (batched) into staging, scatter, per-layer event
+        T->any_in = n_in > 0;
+        std::vector<void*> dst, src;
+        std::vector<size_t> sz;
+        for (int32_t l = 0; l < T->n_layer; ++l) {
+            if (n_in > 0) {
+                dst.clear();
+                src.clear();
+                sz.clear();
+                uint8_t* stage_l = T->stage_in + static_cast<int64_t>(l) * n_in * 2 * pb;
+                for (int64_t i = 0; i < n_in; ++i) {
+                    dst.push_back(stage_l + i * 2 * pb);
+                    src.push_back(T->host + static_cast<int64_t>(in_moves[i].src_slot) * T->chunk_bytes() +
+                                  static_cast<int64_t>(l) * 2 * pb);
+                    sz.push_back(static_cast<size_t>(2 * pb));
+                }
+                copy_batch(dst, src, sz, xs);
+                const int grid = static_cast<int>(std::min<int64_t>(n_in * 2, n_sms() * 4));
+                swap_scatter_layer_kernel<<<grid, 256, 0, xs>>>(stage_l, kp + l * layer_stride, vp + l * layer_stride, pb,
+                                                               T->d_slots + T->max_chunks, static_cast<int32_t>(n_in));
+                cuda_check(cudaGetLastError(), "swap scatter");
+                count_launch();
+            }
+            cuda_check(cudaEventRecord(T->layer_ready[static_cast<size_t>(l)], xs), "event record");
+        }
+        // 3. swap-out D2H behind the swap-ins on the copy stream (no duplex contention)
+        if (n_out > 0) {
+            dst.clear();
+            src.clear();
+            sz.clear();
+            for (int64_t i = 0; i < n_out; ++i) {
+                dst.push_back(T->host + static_cast<int64_t>(out_moves[i].dst_slot) * T->chunk_bytes());
+                src.push_back(T->stage_out + i * T->chunk_bytes());
+                sz.push_back(static_cast<size_t>(T->chunk_bytes()));
+            }
+            copy_batch(dst, src, sz, xs);
+        }
+        cuda_check(cudaEventRecord(T->done, xs), "event record");
+    });
+}
+
+pb_status pb_swap_wait_layer(pb_kv_tier* T, int32_t layer, void* compute_stream) {
+    return guarded([&] {
+        if (!T || layer < 0 || layer >= T->n_layer) fail(PB_ERR_DIMENSION_MISMATCH, "layer out of range");
+        cuda_check(cudaStreamWaitEvent(as_stream(compute_stream), T->layer_ready[static_cast<size_t>(layer)], 0),
+                   "stream wait");
+    });
+}
+
+pb_status pb_swap_sync(pb_kv_tier* T) {
+    return guarded([&] {
+        if (!T) fail(PB_ERR_ERROR, "null tier");
+        cuda_check(cudaEventSynchronize(T->done), "swap sync");
+    });
+}
+
+} // extern "C"

@@ -1,0 +1,95 @@
+"""CPU-tier swap engine (pb_swap_step): bytes land where the bookkeeping's slot moves say,
+bit-exact, with the reference's ordering contract (src/swap_engine.cpp:21-53) and the
+same-step slot-reuse hazards of the LIFO reclaim (src/paged_kv_cache.cpp:28-37) handled."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+from paper_2312_05516_b200.abi import KvCache, KvTier  # noqa: E402
+
+
+def _pools(torch, n_layer, n_slots, page_bytes, seed):
+    g = torch.Generator(device="cuda").manual_seed(seed)
+    k = torch.randint(0, 256, (n_layer, n_slots, page_bytes), dtype=torch.uint8, device="cuda", generator=g)
+    v = torch.randint(0, 256, (n_layer, n_slots, page_bytes), dtype=torch.uint8, device="cuda", generator=g)
+    return k, v
+
+
+def test_swap_out_then_in_roundtrip(cuda):
+    torch = cuda
+    L, n_slots, page = 3, 24, 16 * 2 * 128 * 2
+    k, v = _pools(torch, L, n_slots, page, 1)
+    k0, v0 = k.cpu().numpy().copy(), v.cpu().numpy().copy()
+    tier = KvTier(L, 16, page, 8)
+    cs, xs = torch.cuda.Stream(), torch.cuda.Stream()
+    out = [(100, 3, 5), (101, 7, 0), (102, 20, 9)]  # chunk, device src -> host dst
+    tier.step(k.data_ptr(), v.data_ptr(), n_slots * page, out, [], cs.cuda_stream, xs.cuda_stream)
+    tier.sync()
+    host = tier.host_view().reshape(16, L, 2, page)
+    for _, d, h in out:
+        for l in range(L):
+            assert np.array_equal(host[h, l, 0], k0[l, d]) and np.array_equal(host[h, l, 1], v0[l, d])
+    # swap back into different device slots, layer by layer
+    back = [(100, 5, 11), (101, 0, 12), (102, 9, 13)]  # host src -> device dst
+    tier.step(k.data_ptr(), v.data_ptr(), n_slots * page, [], back, cs.cuda_stream, xs.cuda_stream)
+    for l in range(L):
+        tier.wait_layer(l, cs.cuda_stream)
+    torch.cuda.synchronize()
+    kn, vn = k.cpu().numpy(), v.cpu().numpy()
+    for (_, d, _h), (_, _h2, dd) in zip(out, back):
+        for l in range(L):
+            assert np.array_equal(kn[l, dd], k0[l, d]) and np.array_equal(vn[l, dd], v0[l, d])
+
+
+def test_same_step_slot_reuse_hazard(cuda):
+    """A device slot vacated by swap-out is refilled by a swap-in in the SAME step (the LIFO
+    reclaim makes this common): the host must get the old bytes, the device the new ones."""
+    torch = cuda
+    L, n_slots, page = 4, 8, 4096
+    k, v = _pools(torch, L, n_slots, page, 2)
+    k0, v0 = k.cpu().numpy().copy(), v.cpu().numpy().copy()
+    tier = KvTier(L, 4, page, 4)
+    host = tier.host_view().reshape(4, L, 2, page)
+    rng = np.random.default_rng(3)
+    host[2] = rng.integers(0, 256, size=(L, 2, page), dtype=np.uint8)  # chunk resident on host slot 2
+    incoming = host[2].copy()
+    cs, xs = torch.cuda.Stream(), torch.cuda.Stream()
+    # evict device slot 6 -> host slot 1, restore host slot 2 -> device slot 6 (same step)
+    tier.step(k.data_ptr(), v.data_ptr(), n_slots * page, [(7, 6, 1)], [(9, 2, 6)], cs.cuda_stream, xs.cuda_stream)
+    for l in range(L):
+        tier.wait_layer(l, cs.cuda_stream)
+    tier.sync()
+    torch.cuda.synchronize()
+    for l in range(L):
+        assert np.array_equal(host[1, l, 0], k0[l, 6]) and np.array_equal(host[1, l, 1], v0[l, 6])
+        assert np.array_equal(k.cpu().numpy()[l, 6], incoming[l, 0])
+        assert np.array_equal(v.cpu().numpy()[l, 6], incoming[l, 1])
+
+
+def test_cache_moves_drive_the_engine(cuda):
+    """Bookkeeping -> bytes: moves reported by pb_cache_* are executed by pb_swap_step and
+    every chunk's bytes follow it through evict -> restore cycles."""
+    torch = cuda
+    L, dev_slots, host_slots, page = 2, 12, 12, 2048
+    cache = KvCache(16, dev_slots, host_slots)
+    k, v = _pools(torch, L, dev_slots, page, 4)
+    tier = KvTier(L, host_slots, page, dev_slots)
+    cs, xs = torch.cuda.Stream(), torch.cuda.Stream()
+    ids = cache.allocate(1, 16 * 6, 0.0) + cache.allocate(2, 16 * 4, 0.0)
+    truth = {c: (k.cpu().numpy()[:, cache.chunk(c).slot].copy(), v.cpu().numpy()[:, cache.chunk(c).slot].copy())
+             for c in ids}
+    out = cache.apply_evictions(ids[:5], True)
+    ids3 = cache.allocate(3, 16 * 5, 1.0)  # reuses the vacated slots (LIFO) in the same step
+    tier.step(k.data_ptr(), v.data_ptr(), dev_slots * page, out, [], cs.cuda_stream, xs.cuda_stream)
+    tier.sync()
+    assert len(ids3) == 5
+    cache.release_conversation(3)
+    back = cache.restore(ids[:5])
+    tier.step(k.data_ptr(), v.data_ptr(), dev_slots * page, [], back, cs.cuda_stream, xs.cuda_stream)
+    tier.sync()
+    torch.cuda.synchronize()
+    kn, vn = k.cpu().numpy(), v.cpu().numpy()
+    for c in ids[:5]:
+        s = cache.chunk(c).slot
+        assert np.array_equal(kn[:, s], truth[c][0]) and np.array_equal(vn[:, s], truth[c][1])
