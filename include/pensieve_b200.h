@@ -272,6 +272,56 @@ pb_status pb_cache_verify(const pb_kv_cache* cache);
 /* dump() text; returns its length, writes at most cap-1 chars  paged_kv_cache.cpp:314-339 */
 int64_t pb_cache_dump(const pb_kv_cache* cache, char* buf, int64_t cap);
 
+/* ===================================================================== step planner
+ * The reference Scheduler (include/kvsim/scheduler.hpp:88-179, src/scheduler.cpp) over a
+ * pb_kv_cache: FCFS admission with reserve, prefix-drop span construction
+ * (plan_request :162-230), rematerialize -> restore -> allocate (commit_admission
+ * :232-258), eviction with host-overflow drops (:71-160), suspension (:292-350) and batch
+ * assembly (build_batch :352-420).  Spans and block tables are bit-identical to the
+ * reference; every plan also carries the slot moves for pb_swap_step. */
+typedef struct pb_scheduler pb_scheduler;
+typedef struct pb_sched_params { /* SchedulerParams, scheduler.hpp:75-82 */
+    int32_t split_mode; /* 0 unified (prefill + decode in one plan), 1 split */
+    int32_t policy;     /* 0 pensieve retention value, 1 LRU */
+    int32_t stateful;   /* retain KV across turns */
+    int64_t token_budget;
+    double swap_threshold;
+    double reserve_fraction;
+} pb_sched_params;
+void pb_sched_default_params(pb_sched_params* params);
+/* cost profile: anchors (context_len, seconds per 32-token chunk), cost_model.hpp:170-177 */
+pb_status pb_sched_create(pb_kv_cache* cache, const int64_t* anchor_len, const double* anchor_sec,
+                          int32_t n_anchors, double c_other, double per_token_other,
+                          const pb_sched_params* params, pb_scheduler** out);
+/* synthetic_profile(k_attn, ...), cost_model.cpp:77-85 */
+pb_status pb_sched_create_synthetic(pb_kv_cache* cache, double k_attn, double c_other,
+                                    double per_token_other, const pb_sched_params* params,
+                                    pb_scheduler** out);
+void pb_sched_destroy(pb_scheduler* sched);
+pb_status pb_sched_enqueue(pb_scheduler* sched, int64_t req_id, int64_t conv_id, int32_t turn,
+                           double arrival, int64_t prompt, int64_t output);
+pb_status pb_sched_append_history(pb_scheduler* sched, int64_t conv, int64_t tokens);
+/* begin_step -> maybe_swap_out -> admit -> ensure_generation_capacity -> build_batch */
+pb_status pb_sched_step(pb_scheduler* sched, double now, int32_t* n_plans);
+/* info[8]: n_spans, total tokens, block-table entries, swap_in, swap_out, recompute tokens,
+ * in_moves, out_moves */
+pb_status pb_sched_plan_info(const pb_scheduler* sched, int32_t plan, int64_t* info8);
+pb_status pb_sched_plan_spans(const pb_scheduler* sched, int32_t plan, int64_t* req_id,
+                              int64_t* query_start, int64_t* query_len, int64_t* context_len,
+                              int64_t* causal_offset, int32_t* block_tables, int64_t* bt_offsets);
+pb_status pb_sched_plan_moves(const pb_scheduler* sched, int32_t plan, pb_slot_move* in_moves,
+                              pb_slot_move* out_moves);
+/* complete_plan(plan, end_time)                                 scheduler.cpp:433-457 */
+pb_status pb_sched_complete(pb_scheduler* sched, int32_t plan, double end_time, int64_t* finished,
+                            int64_t cap, int64_t* n_finished);
+/* plan_request without mutation; info[9] = input, recompute, pending, n_rematerialize,
+ * n_swap_in, append_slots, device_hit, host_hit, n_spans; spans as (q_len, ctx, offset) */
+pb_status pb_sched_plan_request(const pb_scheduler* sched, int64_t req_id, int64_t conv_id,
+                                int64_t prompt, int64_t output, int64_t generated,
+                                int32_t suspended, int64_t* info9, int64_t* span3, int64_t cap);
+int64_t pb_sched_queue_size(const pb_scheduler* sched);
+int64_t pb_sched_running_size(const pb_scheduler* sched);
+
 #ifdef __cplusplus
 } /* extern "C" */
 #endif

@@ -348,6 +348,8 @@ struct pb_kv_cache {
     PagedKvCache cache;
 };
 
+PagedKvCache& pb_cache_impl(pb_kv_cache* c) { return c->cache; }
+
 namespace {
 
 template <class V> void copy_out(const V& v, typename V::value_type* out, int64_t cap, int64_t* n) {

@@ -103,3 +103,6 @@ private:
 };
 
 } // namespace pb
+
+struct pb_kv_cache;
+pb::PagedKvCache& pb_cache_impl(pb_kv_cache* c); // C-ABI handle -> C++ object
