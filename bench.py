@@ -200,8 +200,11 @@ def bench_ours(args):
     if w.n_kv_head % world:
         raise SystemExit(f"n_kv_head {w.n_kv_head} not divisible by {world} ranks")
     nkv = w.n_kv_head // world
-    shape = w.shape(n_kv_head=nkv)
-    batch = w.batch()
+    # every rank gets rank 0's span/block-table descriptors (the same migration plan,
+    # PAPER.md:741-744) and its own kv-head shard; no collective touches the attention
+    from paper_2312_05516_b200.sharding import broadcast_batch, shard_shape
+    shape = shard_shape(w.shape(), rank, world)
+    batch = broadcast_batch(w.batch() if rank == 0 else None) if world > 1 else w.batch()
     dt = torch.bfloat16 if w.dtype == PB_BF16 else torch.float32
     eb = 2 if w.dtype == PB_BF16 else 4
     row = nkv * w.head_size

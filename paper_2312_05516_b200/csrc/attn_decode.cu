@@ -34,11 +34,11 @@ namespace {
 
 using namespace pb::sm100;
 
-constexpr int kDecStages = 3;
+constexpr int kDecStages = 2; // page ring depth per warp (1 page in flight while one is consumed)
 constexpr int kMaxGroup = 16;
 
 // warps per CTA (one CTA per SM): as many independent page streams as shared memory allows
-__host__ __device__ constexpr int dec_warps(int G) { return G <= 4 ? 7 : (G <= 8 ? 6 : 4); }
+// (defined after DecWarp: the count is bounded by shared memory and by registers)
 
 __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) { // FFMA2 (sm_100)
     uint64_t d;
@@ -62,6 +62,15 @@ struct __align__(1024) DecWarp {
     uint64_t qfull[kDecStages];
 };
 
+// warps per CTA (one CTA per SM): as many independent page streams as shared memory (227 KB)
+// and the register file allow (the G=8 and G=16 variants need ~250 registers per thread)
+template <int D, int G>
+constexpr int dec_warps() {
+    constexpr int by_smem = static_cast<int>((232448 - 1024) / sizeof(DecWarp<D, G>));
+    constexpr int by_regs = G >= 16 ? 6 : (G >= 8 ? 8 : 12);
+    return by_smem < by_regs ? by_smem : by_regs;
+}
+
 __device__ __forceinline__ float bf_lo(uint32_t x) { return __uint_as_float(x << 16); }
 __device__ __forceinline__ float bf_hi(uint32_t x) { return __uint_as_float(x & 0xffff0000u); }
 
@@ -74,13 +83,13 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 }
 
 template <int D, int G>
-__global__ void __launch_bounds__(dec_warps(G) * 32, 1)
+__global__ void __launch_bounds__(dec_warps<D, G>() * 32, 1)
     attn_decode_kernel(const __grid_constant__ CUtensorMap tm_k, const __grid_constant__ CUtensorMap tm_v,
                        const AttnParams p) {
     constexpr int KH = D / 64;
     constexpr int kChunks = D / 16;       // 16 B chunks per lane and row (D/2 dims)
     constexpr int kDimsPerLane = D / 32;
-    constexpr int kWarps = dec_warps(G);
+    constexpr int kWarps = dec_warps<D, G>();
     constexpr int kFifo = kDecStages + 1;
     using W = DecWarp<D, G>;
     extern __shared__ uint8_t smem_raw[];
@@ -268,24 +277,33 @@ __global__ void __launch_bounds__(dec_warps(G) * 32, 1)
             const int vh = (D == 128) ? (lane >> 4) : 0;
             const int vbyte = (D == 128) ? ((lane & 15) * 8) : (lane * 4);
 #pragma unroll
-            for (int rr = 0; rr < 16; ++rr) {
-                if (rr < valid_rows) {
-                    const uint8_t* src = vpg + vh * 2048 + rr * 128 + ((((vbyte >> 4) ^ (rr & 7)) << 4) | (vbyte & 15));
-                    float2 vv[kDimsPerLane / 2];
-                    if constexpr (kDimsPerLane == 4) {
-                        const uint2 uv = *reinterpret_cast<const uint2*>(src);
-                        vv[0] = make_float2(bf_lo(uv.x), bf_hi(uv.x));
-                        vv[1] = make_float2(bf_lo(uv.y), bf_hi(uv.y));
-                    } else {
-                        const uint32_t uv = *reinterpret_cast<const uint32_t*>(src);
-                        vv[0] = make_float2(bf_lo(uv), bf_hi(uv));
-                    }
+            for (int r4 = 0; r4 < 4; ++r4) {
+                float4 p4[G]; // probabilities of rows 4*r4 .. 4*r4+3, one broadcast LDS.128 per head
 #pragma unroll
-                    for (int j = 0; j < G; ++j) {
-                        if (j < g) {
-                            const float pj = s.pbuf[j][rr];
+                for (int j = 0; j < G; ++j)
+                    if (j < g) p4[j] = *reinterpret_cast<const float4*>(&s.pbuf[j][r4 * 4]);
 #pragma unroll
-                            for (int e = 0; e < kDimsPerLane / 2; ++e) acc[j][e] = ffma2(make_float2(pj, pj), vv[e], acc[j][e]);
+                for (int q = 0; q < 4; ++q) {
+                    const int rr = r4 * 4 + q;
+                    if (rr < valid_rows) {
+                        const uint8_t* src = vpg + vh * 2048 + rr * 128 + ((((vbyte >> 4) ^ (rr & 7)) << 4) | (vbyte & 15));
+                        float2 vv[kDimsPerLane / 2];
+                        if constexpr (kDimsPerLane == 4) {
+                            const uint2 uv = *reinterpret_cast<const uint2*>(src);
+                            vv[0] = make_float2(bf_lo(uv.x), bf_hi(uv.x));
+                            vv[1] = make_float2(bf_lo(uv.y), bf_hi(uv.y));
+                        } else {
+                            const uint32_t uv = *reinterpret_cast<const uint32_t*>(src);
+                            vv[0] = make_float2(bf_lo(uv), bf_hi(uv));
+                        }
+#pragma unroll
+                        for (int j = 0; j < G; ++j) {
+                            if (j < g) {
+                                const float pj = q == 0 ? p4[j].x : q == 1 ? p4[j].y : q == 2 ? p4[j].z : p4[j].w;
+#pragma unroll
+                                for (int e = 0; e < kDimsPerLane / 2; ++e)
+                                    acc[j][e] = ffma2(make_float2(pj, pj), vv[e], acc[j][e]);
+                            }
                         }
                     }
                 }
@@ -380,7 +398,7 @@ int g_dec_sms = 0;
 
 template <int D, int G>
 void launch_decode_t(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st) {
-    const size_t smem = sizeof(DecWarp<D, G>) * dec_warps(G) + 1024;
+    const size_t smem = sizeof(DecWarp<D, G>) * dec_warps<D, G>() + 1024;
     static bool attr = false;
     if (!attr) {
         cuda_check(cudaFuncSetAttribute(attn_decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -393,8 +411,8 @@ void launch_decode_t(const AttnParams& p, const CUtensorMap* maps, cudaStream_t 
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_dec_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int grid = std::max(1, std::min(g_dec_sms, (p.n_items + dec_warps(G) - 1) / dec_warps(G)));
-    attn_decode_kernel<D, G><<<grid, dec_warps(G) * 32, smem, st>>>(maps[1], maps[2], p);
+    const int grid = std::max(1, std::min(g_dec_sms, (p.n_items + dec_warps<D, G>() - 1) / dec_warps<D, G>()));
+    attn_decode_kernel<D, G><<<grid, dec_warps<D, G>() * 32, smem, st>>>(maps[1], maps[2], p);
     cuda_check(cudaGetLastError(), "attn_decode launch");
     count_launch();
 }
