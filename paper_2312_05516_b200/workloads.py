@@ -285,3 +285,40 @@ def random_instance(rng: SplitMix64, n_head: int, n_kv: int, d: int, chunk: int,
             q = 1 + rng.next() % (ctx if max_q is None else min(ctx, max_q))
         convs.append([(ctx - q, q)])
     return _build("random", n_head, n_kv, d, chunk, dtype, rng.seed, convs, rng)
+
+
+# --------------------------------------------------------------------------- config 5
+def sharegpt_trace(n_conv: int, seed: int = 5, mean_turns: float = 5.5, mean_prompt: float = 37.77,
+                   sigma_prompt: float = 0.6, mean_output: float = 204.58, sigma_output: float = 0.5,
+                   max_prompt: int = 512, max_output: int = 2048, max_context: int = 16384):
+    """Synthetic ShareGPT-like multi-turn trace: geometric turn counts, lognormal prompt and
+    output lengths with the ShareGPT statistics the paper reports (the
+    reference's synthetic generator uses the same distribution family and parameters).
+    Returns [(conv_id, [(prompt, output), ...])]."""
+    rng = SplitMix64(seed)
+
+    def normal():
+        u1 = max(rng.u01(), 1e-300)
+        u2 = rng.u01()
+        return math.sqrt(-2.0 * math.log(u1)) * math.cos(2.0 * math.pi * u2)
+
+    def lognormal(mean, sigma):
+        mu = math.log(mean) - 0.5 * sigma * sigma
+        return math.exp(mu + sigma * normal())
+
+    p_stop = 1.0 / mean_turns
+    out = []
+    for c in range(n_conv):
+        turns, total = [], 0
+        while True:
+            pr = max(1, min(max_prompt, int(round(lognormal(mean_prompt, sigma_prompt)))))
+            ou = max(1, min(max_output, int(round(lognormal(mean_output, sigma_output)))))
+            if total + pr + ou > max_context:
+                break
+            turns.append((pr, ou))
+            total += pr + ou
+            if rng.u01() < p_stop:
+                break
+        if turns:
+            out.append((c, turns))
+    return out
