@@ -354,6 +354,155 @@ def bench_ours(args):
     return 0
 
 
+def plan_sharegpt_steps(n_conv: int, n_steps: int, host_factor: float = 0.5, think: float = 1.0):
+    """Config 5: drive the step planner (pb_sched_*) over a synthetic ShareGPT-like trace with
+    the device tier at ~30% of the working set and a host tier small enough to
+    overflow (so leading chunks get dropped and come back as recompute spans); return the
+    planned steps (ragged batch + swap slot moves) starting at the first step that carries a
+    dropped-prefix recompute span (or, failing that, the first swap-in)."""
+    from paper_2312_05516_b200.abi import KvCache
+    from paper_2312_05516_b200.planner import Scheduler, default_params
+    from paper_2312_05516_b200.workloads import sharegpt_trace
+
+    trace = sharegpt_trace(n_conv, seed=5)
+    ws = sum((sum(p + o for p, o in turns) + 15) // 16 for _, turns in trace)
+    dev_slots = max(64, int(0.3 * ws))
+    host_slots = max(1, int(host_factor * dev_slots))
+    cache = KvCache(16, dev_slots, host_slots)
+    sched = Scheduler(cache, params=default_params(token_budget=4096))
+    pending = [(0.02 * c, c, 0) for c, _ in trace]
+    turns = dict(trace)
+    req, req_conv, now, steps, recorded, history = 0, {}, 0.0, 0, [], []
+    while (pending or sched.queue_size or sched.running_size) and steps < 20000 and len(recorded) < n_steps:
+        steps += 1
+        now += 0.05
+        for item in sorted(p for p in pending if p[0] <= now):
+            pending.remove(item)
+            t, c, k = item
+            pr, ou = turns[c][k]
+            sched.enqueue(req, c, t, pr, ou, k)
+            req_conv[req] = (c, k)
+            req += 1
+        plans = sched.step(now)
+        for p in plans:
+            history.append(p)
+            if not recorded and p.recompute_tokens > 0:
+                recorded = history[-1:]
+            elif recorded:
+                recorded.append(p)
+        for i in range(len(plans)):
+            for r in sched.complete(i, now + 0.01):
+                c, k = req_conv[r]
+                if k + 1 < len(turns[c]):
+                    pending.append((now + think, c, k + 1))  # think time
+    if not recorded:  # no drop happened: first returning turn that swaps in
+        first = next((i for i, p in enumerate(history) if p.in_moves), 0)
+        recorded = history[first:first + n_steps]
+    return recorded, dev_slots, host_slots
+
+
+def bench_config5(args):
+    """Config 5: CPU-tier swap-in/out (pb_swap_step, layer-pipelined) + the ragged attention of
+    the same planned steps, Llama-2-13B shape, one GPU."""
+    import torch
+
+    from paper_2312_05516_b200 import abi
+    from paper_2312_05516_b200.abi import PB_BF16, AttentionPlan, AttnShape, KvTier
+
+    n_layer = args.layers or 40
+    n_head, n_kv, d, chunk = 40, 10, 128, 16
+    steps, dev_slots, host_slots = plan_sharegpt_steps(args.c5_convs, args.warmup + args.steps)
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    page_elems = chunk * n_kv * d
+    page_bytes = page_elems * 2
+    k = torch.empty((n_layer, dev_slots, page_elems), dtype=torch.bfloat16, device=dev)
+    v = torch.empty_like(k)
+    abi.fill_unit(k.data_ptr(), PB_BF16, k.numel(), 5, 0)
+    abi.fill_unit(v.data_ptr(), PB_BF16, v.numel(), 5, k.numel())
+    max_tok = max(p.total_tokens for p in steps)
+    q = torch.empty(max_tok * n_head * d, dtype=torch.bfloat16, device=dev)
+    abi.fill_unit(q.data_ptr(), PB_BF16, q.numel(), 6, 0)
+    out = torch.empty_like(q)
+    max_chunks = max(max(len(p.in_moves), len(p.out_moves)) for p in steps) + 1
+    tier = KvTier(n_layer, host_slots, page_bytes, max_chunks)
+    shape = AttnShape(n_head, n_kv, d, chunk, dev_slots, PB_BF16, math.sqrt(d))
+    cs, xs = torch.cuda.Stream(), torch.cuda.Stream()
+    plans = [AttentionPlan(shape, p.batch()) for p in steps]
+    wss = max(pl.workspace_bytes() for pl in plans)
+    wsb = torch.zeros(max(1, wss), dtype=torch.uint8, device=dev)
+    layer_stride = dev_slots * page_bytes
+
+    def run(i, ev=None):
+        p, pl = steps[i], plans[i]
+        if ev:
+            ev[0].record(xs)
+        tier.step(k.data_ptr(), v.data_ptr(), layer_stride, p.out_moves, p.in_moves, cs.cuda_stream, xs.cuda_stream)
+        if ev:
+            ev[1].record(xs)
+        pl.upload(cs.cuda_stream)
+        for l in range(n_layer):
+            tier.wait_layer(l, cs.cuda_stream)
+            pl.run(q.data_ptr(), k.data_ptr() + l * layer_stride, v.data_ptr() + l * layer_stride, out.data_ptr(),
+                   wsb.data_ptr(), cs.cuda_stream)
+
+    for i in range(args.warmup):
+        run(i)
+    torch.cuda.synchronize()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    swap_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clocks = ClockSampler(0)
+    clocks.start()
+    torch.cuda.synchronize()
+    t0.record(cs)
+    for s in range(args.steps):
+        run(args.warmup + s, swap_ev[s])
+    t1.record(cs)
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    total_ms = t0.elapsed_time(t1)
+    swap_ms = sum(a.elapsed_time(b) for a, b in swap_ev)
+    timed = steps[args.warmup:args.warmup + args.steps]
+    attn_bytes = sum(pl.stats()["bytes"] for pl in plans[args.warmup:args.warmup + args.steps]) * n_layer
+    attn_flops = sum(pl.stats()["flops"] for pl in plans[args.warmup:args.warmup + args.steps]) * n_layer
+    n_in = sum(len(p.in_moves) for p in timed)
+    n_out = sum(len(p.out_moves) for p in timed)
+    swap_bytes = (n_in + n_out) * tier.chunk_bytes
+    # pinned-copy peaks on this box (1 GiB each way)
+    big = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
+    hbuf = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
+    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    big.copy_(hbuf, non_blocking=True)
+    torch.cuda.synchronize()
+    e[0].record(); big.copy_(hbuf, non_blocking=True); e[1].record()
+    e[2].record(); hbuf.copy_(big, non_blocking=True); e[3].record()
+    torch.cuda.synchronize()
+    h2d_peak = (1 << 30) / (e[0].elapsed_time(e[1]) / 1e3) / 1e9
+    d2h_peak = (1 << 30) / (e[2].elapsed_time(e[3]) / 1e3) / 1e9
+    peaks, peak_src = load_peaks()
+    value = attn_bytes / (total_ms / 1e3) / 1e9
+    line = {
+        "metric": "config 5: ragged paged-attn GB/s with layer-pipelined CPU-tier swap-in/out",
+        "value": value, "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic ShareGPT-like trace (workloads.sharegpt_trace) planned by pb_sched",
+        "config": {"workload": "cfg5-sharegpt-llama2-13b", "n_layer": n_layer, "conversations": args.c5_convs,
+                   "device_slots": dev_slots, "host_slots": host_slots, "chunk_bytes": tier.chunk_bytes,
+                   "spans_per_step": sum(len(p.spans) for p in timed) / len(timed),
+                   "recompute_tokens": sum(p.recompute_tokens for p in timed)},
+        "roofline": {"bound": "hbm", "achieved": value, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": value / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_src,
+                     "tflops": attn_flops / (total_ms / 1e3) / 1e12},
+        "swap": {"chunks_in": n_in, "chunks_out": n_out, "bytes": swap_bytes,
+                 "copy_stream_gbs": swap_bytes / (swap_ms / 1e3) / 1e9 if swap_ms > 0 else None,
+                 "pinned_h2d_peak_gbs": h2d_peak, "pinned_d2h_peak_gbs": d2h_peak},
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
 def load_traffic(name):
     p = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(p):
@@ -366,12 +515,19 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4])
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5])
     ap.add_argument("--layers", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU reference work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--c5-convs", type=int, default=96, help="config 5: conversations in the trace")
     args = ap.parse_args()
+    if args.config == 5:
+        if args.impl == "reference":
+            print(json.dumps({"impl": "reference", "unavailable": "config 5 has no CPU reference: the "
+                              "reference swap engine moves no bytes (SPEC.md:458)"}))
+            return 0
+        return bench_config5(args)
     if args.impl == "reference":
         return bench_reference(args)
     return bench_ours(args)

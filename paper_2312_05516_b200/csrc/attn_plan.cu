@@ -35,6 +35,8 @@ struct pb_attn_plan {
     std::vector<WorkItem> tc_items;     // prefill tiles for the sm_100a tcgen05 kernel
     std::vector<WorkItem> decode_items; // single-token split-KV units
     bool decode_kernel = false;         // decode units built (else decode spans go SIMT)
+    cudaStream_t side = nullptr;        // decode units overlap the tile kernel tail
+    cudaEvent_t fork = nullptr, join = nullptr;
     int32_t n_groups = 0;
     int32_t n_parts = 0;
     int32_t n_prefill = 0, n_decode = 0, n_split_spans = 0;
@@ -92,9 +94,12 @@ void validate(const pb_attn_shape& s, int32_t n_spans, const int64_t* qs, const 
         if (cl[i] > INT32_MAX / 2) fail(PB_ERR_UNSUPPORTED, "context too long");
 }
 
-// Decode spans longer than this many pages are split across CTAs (split-KV); partial
-// results are merged by the last-arriving split inside the same launch.
-constexpr int kDecodeSplitPages = 64;
+// Decode spans are cut into units of at most split_pages pages (split-KV); partial results
+// are merged by the last-arriving unit inside the same launch.  The unit size adapts to the
+// batch: ~kDecodeUnitsTarget units in total (several per decode warp on 148 SMs, for load
+// balance), never more than 64 pages (the decode kernel caches a unit's block-table slice in
+// two registers per lane) and never fewer than 8.
+constexpr int kDecodeUnitsTarget = 4096;
 
 void build_work(pb_attn_plan& P) {
     const pb_attn_shape& s = P.shape;
@@ -106,6 +111,10 @@ void build_work(pb_attn_plan& P) {
     const int tc_tokens = tc ? sm100_tile_tokens(g) : 0;
     P.decode_kernel = tc && decode_supports(s.head_size, s.chunk_size, g);
     std::vector<std::pair<double, WorkItem>> tc_list, dec_list;
+    int64_t decode_pages = 0;
+    for (const SpanDev& sp : P.spans)
+        if (sp.query_len == 1) decode_pages += static_cast<int64_t>(sp.n_pages) * s.n_kv_head;
+    const int split_pages = static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(64, decode_pages / kDecodeUnitsTarget)));
     for (int32_t si = 0; si < static_cast<int32_t>(P.spans.size()); ++si) {
         const SpanDev& sp = P.spans[si];
         if (sp.query_len == 0) continue;
@@ -147,7 +156,7 @@ void build_work(pb_attn_plan& P) {
                 const int pages = sp.n_pages;
                 const int n_parts = (P.flags & PB_PLAN_NO_SPLIT)
                                         ? 1
-                                        : std::max(1, (pages + kDecodeSplitPages - 1) / kDecodeSplitPages);
+                                        : std::max(1, (pages + split_pages - 1) / split_pages);
                 const int per = (pages + n_parts - 1) / n_parts;
                 int group_id = -1, part_base = 0;
                 if (n_parts > 1) {
@@ -350,6 +359,22 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
             ps.n_items = static_cast<int32_t>(P->simt_items.size());
             launch_attn_simt(ps, P->shape.dtype, ps.n_items, st);
         }
+        // Tensor-bound tiles and HBM-bound decode units of the same batch: the decode kernel
+        // is forked onto a side stream so its persistent CTAs take SMs as soon as tile CTAs
+        // retire (the tile kernel's tail) and the two bottlenecks overlap; joined back before
+        // pb_attn_run's stream continues.
+        const bool both = !P->tc_items.empty() && !P->decode_items.empty();
+        cudaStream_t dst = st;
+        if (both) {
+            if (!P->side) {
+                cuda_check(cudaStreamCreateWithFlags(&P->side, cudaStreamNonBlocking), "side stream");
+                cuda_check(cudaEventCreateWithFlags(&P->fork, cudaEventDisableTiming), "event");
+                cuda_check(cudaEventCreateWithFlags(&P->join, cudaEventDisableTiming), "event");
+            }
+            cuda_check(cudaEventRecord(P->fork, st), "fork");
+            cuda_check(cudaStreamWaitEvent(P->side, P->fork, 0), "fork wait");
+            dst = P->side;
+        }
         if (!P->tc_items.empty()) {
             AttnParams pt = p;
             pt.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_tc);
@@ -360,7 +385,11 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
             AttnParams pd = p;
             pd.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_dec);
             pd.n_items = static_cast<int32_t>(P->decode_items.size());
-            launch_attn_decode(pd, P->shape, P->sm100, P->total_tokens, st);
+            launch_attn_decode(pd, P->shape, P->sm100, P->total_tokens, dst);
+        }
+        if (both) {
+            cuda_check(cudaEventRecord(P->join, P->side), "join");
+            cuda_check(cudaStreamWaitEvent(st, P->join, 0), "join wait");
         }
     });
 }
@@ -380,6 +409,12 @@ void pb_attn_plan_destroy(pb_attn_plan* P) {
     if (!P) return;
     if (P->d_buf) cudaFree(P->d_buf);
     sm100_cache_release(P->sm100);
+    if (P->side) {
+        cudaStreamSynchronize(P->side);
+        cudaStreamDestroy(P->side);
+        cudaEventDestroy(P->fork);
+        cudaEventDestroy(P->join);
+    }
     delete P;
 }
 

@@ -293,26 +293,32 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool grow = mt > m_run + kRescaleThreshold;
                 const float m_new = grow ? mt : m_run;
                 const float corr = grow ? ex2(m_run - m_new) : 1.f;
-                float ps[8];
+                float2 ps[4];
 #pragma unroll
-                for (int u = 0; u < 8; ++u) ps[u] = 0.f;
+                for (int u = 0; u < 4; ++u) ps[u] = make_float2(0.f, 0.f);
                 uint32_t pk0[32], pk1[32];
+                const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_new, -m_new);
 #pragma unroll
                 for (int c = 0; c < 128; c += 2) {
-                    // exp((s - max) / scale) in base 2; one pair in four on the FMA pipe (cubic),
-                    // the rest on MUFU, so the two softmax groups do not saturate MUFU
-                    const float a0 = fmaf(x[c], sl2, -m_new), a1 = fmaf(x[c + 1], sl2, -m_new);
-                    const bool poly = ((c >> 1) & 3) == 3;
-                    const float e0 = poly ? exp2_poly3(a0) : ex2(a0);
-                    const float e1 = poly ? exp2_poly3(a1) : ex2(a1);
-                    ps[c & 7] += e0;
-                    ps[(c + 1) & 7] += e1;
-                    if (c < 64) pk0[c >> 1] = pack_bf16x2(e0, e1);
-                    else pk1[(c - 64) >> 1] = pack_bf16x2(e0, e1);
+                    // exp((s - max) / scale) in base 2 on packed pairs (FFMA2/FADD2); every other
+                    // pair on the FMA pipe (cubic), the rest on MUFU, so the two softmax groups
+                    // sharing an SMSP do not saturate MUFU
+                    const float2 a = fma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
+                    float2 e;
+                    if ((c >> 1) & 1) {
+                        e = exp2_poly3_x2(a);
+                    } else {
+                        e.x = ex2(a.x);
+                        e.y = ex2(a.y);
+                    }
+                    ps[(c >> 1) & 3] = add2(ps[(c >> 1) & 3], e);
+                    if (c < 64) pk0[c >> 1] = pack_bf16x2(e.x, e.y);
+                    else pk1[(c - 64) >> 1] = pack_bf16x2(e.x, e.y);
                     if (c == 62) tmem_st32(t_lane + col_s, pk0); // P over the first 64 columns of S_t
                 }
                 tmem_st32(t_lane + col_s + 32, pk1);
-                const float sum = ((ps[0] + ps[1]) + (ps[2] + ps[3])) + ((ps[4] + ps[5]) + (ps[6] + ps[7]));
+                const float2 s2 = add2(add2(ps[0], ps[1]), add2(ps[2], ps[3]));
+                const float sum = s2.x + s2.y;
                 l_run = l_run * corr + sum;
                 m_run = m_new;
                 // S_t(j) landing implies PV_t(j-1) completed (in-order tensor pipe, the commit for

@@ -177,6 +177,43 @@ __device__ __forceinline__ float exp2_poly3(float x) {
     return x < -126.f ? 0.f : y;
 }
 
+// ---- packed fp32x2 math (sm_100: FFMA2 / FADD2 / FMUL2 issue two lanes per instruction)
+__device__ __forceinline__ uint64_t f2_bits(float2 v) { return *reinterpret_cast<uint64_t*>(&v); }
+__device__ __forceinline__ float2 bits_f2(uint64_t v) { return *reinterpret_cast<float2*>(&v); }
+__device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) {
+    uint64_t d;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)), "l"(f2_bits(c)));
+    return bits_f2(d);
+}
+__device__ __forceinline__ float2 add2(float2 a, float2 b) {
+    uint64_t d;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return bits_f2(d);
+}
+__device__ __forceinline__ float2 mul2(float2 a, float2 b) {
+    uint64_t d;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
+    return bits_f2(d);
+}
+
+// exp2_poly3 on a pair, with packed fp32x2 arithmetic
+__device__ __forceinline__ float2 exp2_poly3_x2(float2 x) {
+    const float2 xc = make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f));
+    const float2 magic = make_float2(12582912.f, 12582912.f);
+    const float2 r = add2(xc, magic);
+    const float2 rounded = add2(r, make_float2(-12582912.f, -12582912.f));
+    const float2 f = fma2(rounded, make_float2(-1.f, -1.f), xc); // xc - round(xc) in [-0.5, 0.5]
+    float2 p = fma2(make_float2(0.05324155f, 0.05324155f), f, make_float2(0.24228422f, 0.24228422f));
+    p = fma2(p, f, make_float2(0.69354963f, 0.69354963f));
+    p = fma2(p, f, make_float2(0.9999545f, 0.9999545f));
+    float2 y;
+    y.x = __int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23));
+    y.y = __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23));
+    y.x = x.x < -126.f ? 0.f : y.x;
+    y.y = x.y < -126.f ? 0.f : y.y;
+    return y;
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
