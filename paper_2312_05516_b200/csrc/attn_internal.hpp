@@ -56,6 +56,7 @@ struct AttnParams {
     float* part_ml;          // [n_parts][group][2] running max (log2 domain) and sum
     float* part_o;           // [n_parts][group][head_size] unnormalised outputs
     int32_t* work_counter;   // persistent-kernel ticket (self-resetting)
+    int32_t ablate;          // profiling only (PB_ABLATE): 1 skip softmax math, 2 skip exp
 };
 
 } // namespace pb

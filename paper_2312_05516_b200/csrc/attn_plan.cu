@@ -10,6 +10,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <memory>
 #include <mutex>
@@ -347,6 +348,11 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
             fail(PB_ERR_ERROR, "workspace required");
         cudaStream_t st = as_stream(stream);
         AttnParams p = make_params(P, q, k_pages, v_pages, out, workspace);
+        static const int ablate = [] {
+            const char* e = std::getenv("PB_ABLATE");
+            return e ? std::atoi(e) : 0;
+        }();
+        p.ablate = ablate;
         if (workspace && workspace != P->last_workspace) {
             // counters are self-resetting; zero them once per workspace buffer
             cuda_check(cudaMemsetAsync(workspace, 0, 256 + align_up(sizeof(int32_t) * P->n_groups, 256), st),

@@ -272,6 +272,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&s.s_full[t], n_s & 1);
                 ++n_s;
                 tc_fence_after();
+                if (p.ablate == 1) { // profiling: tensor-core + pipeline bound (P left as S bits)
+                    tc_fence_before();
+                    mbar_arrive(&s.p_full[t]);
+                    l_run = 1.f;
+                    continue;
+                }
                 float x[128];
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
@@ -305,7 +311,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // sharing an SMSP do not saturate MUFU
                     const float2 a = fma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
                     float2 e;
-                    if ((c >> 1) & 1) {
+                    if (p.ablate == 2) { // profiling: no exponentials
+                        e = a;
+                    } else if ((c >> 1) & 1) {
                         e = exp2_poly3_x2(a);
                     } else {
                         e.x = ex2(a.x);
