@@ -14,6 +14,11 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(HERE, "libpensieve_b200.so")
+# profiling experiments only: PB_LIB names an alternate in-tree build of the same library
+# (scripts/build_variants.sh); the product always loads SO_PATH
+if os.environ.get("PB_LIB"):
+    _v = os.environ["PB_LIB"]
+    SO_PATH = os.path.join(HERE, "variants", _v if _v.endswith(".so") else _v + ".so")
 
 PB_F32 = 0
 PB_BF16 = 1

@@ -353,6 +353,11 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
             return e ? std::atoi(e) : 0;
         }();
         p.ablate = ablate;
+        // profiling only (PB_ONLY): 1 = run only the tile kernel, 2 = only the decode kernel
+        static const int only = [] {
+            const char* e = std::getenv("PB_ONLY");
+            return e ? std::atoi(e) : 0;
+        }();
         if (workspace && workspace != P->last_workspace) {
             // counters are self-resetting; zero them once per workspace buffer
             cuda_check(cudaMemsetAsync(workspace, 0, 256 + align_up(sizeof(int32_t) * P->n_groups, 256), st),
@@ -369,7 +374,9 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
         // is forked onto a side stream so its persistent CTAs take SMs as soon as tile CTAs
         // retire (the tile kernel's tail) and the two bottlenecks overlap; joined back before
         // pb_attn_run's stream continues.
-        const bool both = !P->tc_items.empty() && !P->decode_items.empty();
+        const bool run_tc = !P->tc_items.empty() && only != 2;
+        const bool run_dec = !P->decode_items.empty() && only != 1;
+        const bool both = run_tc && run_dec;
         cudaStream_t dst = st;
         if (both) {
             if (!P->side) {
@@ -381,13 +388,13 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
             cuda_check(cudaStreamWaitEvent(P->side, P->fork, 0), "fork wait");
             dst = P->side;
         }
-        if (!P->tc_items.empty()) {
+        if (run_tc) {
             AttnParams pt = p;
             pt.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_tc);
             pt.n_items = static_cast<int32_t>(P->tc_items.size());
             launch_attn_sm100(pt, P->shape, P->sm100, P->total_tokens, st);
         }
-        if (!P->decode_items.empty()) {
+        if (run_dec) {
             AttnParams pd = p;
             pd.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_dec);
             pd.n_items = static_cast<int32_t>(P->decode_items.size());

@@ -44,8 +44,25 @@ constexpr int kThreads = 384; // WG0/WG1 softmax of tiles A/B, WG2: TMA warp, MM
 constexpr int kTileRows = 128;        // M rows per query tile and kv rows per kv tile
 constexpr uint32_t kTmemCols = 512;   // S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
 constexpr uint32_t kColO = 256;
-constexpr bool kUseSetMaxNReg = false;
+#ifndef PB_SETMAXNREG
+#define PB_SETMAXNREG 1 // 1: rebalance registers, WG2 (TMA + MMA warps) down, softmax groups up
+#endif
+constexpr bool kUseSetMaxNReg = PB_SETMAXNREG != 0;
+#ifndef PB_REG_LO
+#define PB_REG_LO 88  // WG2 after setmaxnreg.dec
+#endif
+#ifndef PB_REG_HI
+#define PB_REG_HI 208 // softmax groups after setmaxnreg.inc (128*LO + 256*HI <= 64K)
+#endif
 constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max grows by > 2^8
+#ifndef PB_POLY_EVERY
+#define PB_POLY_EVERY 0 // one exp2 pair in N on the FMA pipe; 0 = all on MUFU (measured fastest, see profiles/)
+#endif
+#ifndef PB_LD_SPLIT
+#define PB_LD_SPLIT 0   // 1: overlap the second half of the S read with the first half's max
+#endif
+
+constexpr int kItemRing = 4; // work items fetched ahead by the TMA warp
 
 template <int D>
 struct __align__(1024) Smem {
@@ -55,6 +72,8 @@ struct __align__(1024) Smem {
     uint64_t q_full, q_empty;
     uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
     uint64_t s_full[2], p_full[2], o_ready[2], o_empty[2]; // per query tile
+    uint64_t item_full[kItemRing], item_empty[kItemRing];   // dynamic tile scheduler ring
+    int32_t item_ring[kItemRing];
     uint32_t tmem_base;
 };
 
@@ -116,6 +135,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_init(&s.o_ready[i], 1);
             mbar_init(&s.o_empty[i], 128);
         }
+        for (int i = 0; i < kItemRing; ++i) {
+            mbar_init(&s.item_full[i], 1);
+            mbar_init(&s.item_empty[i], 1 + 8); // MMA thread + the 8 softmax warps
+        }
         mbar_fence_init();
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_k);
@@ -127,9 +150,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     tc_fence_after();
     const uint32_t tmem = s.tmem_base;
     const int wg = warp >> 2;
-    if (kUseSetMaxNReg && wg == 2) asm volatile("setmaxnreg.dec.sync.aligned.u32 112;" ::: "memory");
-    else if (kUseSetMaxNReg) asm volatile("setmaxnreg.inc.sync.aligned.u32 200;" ::: "memory");
-
+    if (wg == 2) {
+    if (kUseSetMaxNReg) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PB_REG_LO) : "memory");
     if (warp == 8) {
         // ============================ TMA producer ============================
         if (elect_one()) {
@@ -137,7 +159,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t kph = 0, vph = 0;
             const uint32_t q_bytes = KH * 128u * static_cast<uint32_t>(g * tpt);
             const int oob_row = p.n_slots * chunk;
-            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+            // Dynamic tile scheduler: the TMA warp takes the next item (items are in LPT order)
+            // from a global ticket when it is ready to load it, and hands the index to the MMA
+            // and softmax roles through a small shared ring.
+            int* ticket = p.work_counter + 2; // [2] next item, [3] retired CTAs (self-resetting)
+            for (;; ++it) {
+                const int slot = it % kItemRing;
+                if (it >= kItemRing) mbar_wait(&s.item_empty[slot], ((it / kItemRing) - 1) & 1);
+                int item = atomicAdd(ticket, 1);
+                if (item >= p.n_items) item = -1;
+                s.item_ring[slot] = item;
+                mbar_arrive(&s.item_full[slot]);
+                if (item < 0) break;
                 const WorkItem w = p.items[item];
                 const SpanDev sp = p.spans[w.span];
                 const ItemTiles T = item_tiles(w, sp, tpt);
@@ -171,6 +204,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
+            // the last CTA to retire re-arms the ticket for the next launch
+            __threadfence();
+            if (atomicAdd(ticket + 1, 1) == static_cast<int>(gridDim.x) - 1) {
+                ticket[0] = 0;
+                ticket[1] = 0;
+            }
         }
     } else if (warp == 9) {
         // ============================ MMA issuer =============================
@@ -180,7 +219,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             int it = 0, kst = 0, vst = 0;
             uint32_t kph = 0, vph = 0;
             uint32_t n_p[2] = {0, 0}, n_oe[2] = {0, 0};
-            for (int item = blockIdx.x; item < p.n_items; item += gridDim.x, ++it) {
+            for (;; ++it) {
+                const int slot = it % kItemRing;
+                mbar_wait(&s.item_full[slot], (it / kItemRing) & 1);
+                const int item = *reinterpret_cast<volatile int32_t*>(&s.item_ring[slot]);
+                mbar_arrive(&s.item_empty[slot]);
+                if (item < 0) break;
                 const WorkItem w = p.items[item];
                 const SpanDev sp = p.spans[w.span];
                 const ItemTiles T = item_tiles(w, sp, tpt);
@@ -246,7 +290,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                 umma_commit(&s.q_empty);
             }
         }
-    } else if (wg < 2) {
+    }
+    } else {
+        if (kUseSetMaxNReg) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(PB_REG_HI) : "memory");
         // ============ softmax / correction / epilogue (one group per query tile) ============
         const int t = wg;                           // query tile of this warpgroup
         const int quad = warp & 3;                  // TMEM lane quadrant of this warp
@@ -257,7 +303,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const float sl2 = p.scale_log2;
         uint32_t n_s = 0, n_o = 0;
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
-        for (int item = blockIdx.x; item < p.n_items; item += gridDim.x) {
+        for (int it = 0;; ++it) {
+            const int slot = it % kItemRing;
+            mbar_wait(&s.item_full[slot], (it / kItemRing) & 1);
+            const int item = *reinterpret_cast<volatile int32_t*>(&s.item_ring[slot]);
+            __syncwarp();
+            if ((threadIdx.x & 31) == 0) mbar_arrive(&s.item_empty[slot]);
+            if (item < 0) break;
             const WorkItem w = p.items[item];
             const SpanDev sp = p.spans[w.span];
             const ItemTiles T = item_tiles(w, sp, tpt);
@@ -279,21 +331,49 @@ __global__ void __launch_bounds__(kThreads, 1)
                     continue;
                 }
                 float x[128];
+                const int kv0 = j * kTileRows;
+                const bool diag = kv0 + kTileRows > allowed;
+                float pm[8];
+#if PB_LD_SPLIT
+                // two halves: the second half's TMEM read is in flight while the first half's
+                // max runs (the wait carries the registers so no use is hoisted above it)
+                tmem_ld32(t_lane + col_s, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
+                tmem_ld32(t_lane + col_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&x[32]));
+                tmem_ld_wait_dep(*reinterpret_cast<uint32_t(*)[32]>(&x[0]));
+                tmem_ld_wait_dep(*reinterpret_cast<uint32_t(*)[32]>(&x[32]));
+                tmem_ld32(t_lane + col_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&x[64]));
+                tmem_ld32(t_lane + col_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&x[96]));
+                if (diag) {
+#pragma unroll
+                    for (int c = 0; c < 64; ++c) x[c] = (kv0 + c < allowed) ? x[c] : -CUDART_INF_F;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) pm[u] = x[u];
+#pragma unroll
+                for (int c = 8; c < 64; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
+                tmem_ld_wait_dep(*reinterpret_cast<uint32_t(*)[32]>(&x[64]));
+                tmem_ld_wait_dep(*reinterpret_cast<uint32_t(*)[32]>(&x[96]));
+                if (diag) {
+#pragma unroll
+                    for (int c = 64; c < 128; ++c) x[c] = (kv0 + c < allowed) ? x[c] : -CUDART_INF_F;
+                }
+#pragma unroll
+                for (int c = 64; c < 128; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
+#else
 #pragma unroll
                 for (int c = 0; c < 4; ++c)
                     tmem_ld32(t_lane + col_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
                 tmem_ld_wait();
                 // causal mask (only tiles that cross this row's boundary) + running max
-                const int kv0 = j * kTileRows;
-                if (kv0 + kTileRows > allowed) {
+                if (diag) {
 #pragma unroll
                     for (int c = 0; c < 128; ++c) x[c] = (kv0 + c < allowed) ? x[c] : -CUDART_INF_F;
                 }
-                float pm[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) pm[u] = x[u];
 #pragma unroll
                 for (int c = 8; c < 128; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
+#endif
                 const float mt = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
                                        fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * sl2;
                 const bool grow = mt > m_run + kRescaleThreshold;
@@ -313,7 +393,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float2 e;
                     if (p.ablate == 2) { // profiling: no exponentials
                         e = a;
-                    } else if ((c >> 1) & 1) {
+                    } else if (PB_POLY_EVERY > 0 && ((c >> 1) % (PB_POLY_EVERY > 0 ? PB_POLY_EVERY : 1)) ==
+                                                        PB_POLY_EVERY - 1) {
                         e = exp2_poly3_x2(a);
                     } else {
                         e.x = ex2(a.x);
