@@ -224,7 +224,7 @@ def bench_ours(args):
     out = torch.empty_like(q)
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
-    plan = AttentionPlan(shape, batch)
+    plan = AttentionPlan(shape, batch, args.plan_flags)
     plan.upload(sh)
     ws = torch.zeros(max(1, plan.workspace_bytes()), dtype=torch.uint8, device=dev)
     stats = plan.stats()
@@ -279,7 +279,7 @@ def bench_ours(args):
     t0 = time.perf_counter()
     e0.record(stream)
     for _ in range(e2e_steps):
-        p2 = AttentionPlan(shape, batch)
+        p2 = AttentionPlan(shape, batch, args.plan_flags)
         p2.upload(sh)
         for l in range(n_layer):
             q.copy_(q_host, non_blocking=True)
@@ -520,6 +520,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU reference work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--plan-flags", type=int, default=int(os.environ.get("PB_PLAN_FLAGS", "0")),
+                    help="pb_attn_plan flags (profiling comparisons)")
     ap.add_argument("--c5-convs", type=int, default=96, help="config 5: conversations in the trace")
     args = ap.parse_args()
     if args.config == 5:

@@ -78,7 +78,8 @@ typedef struct pb_attn_plan pb_attn_plan;
 enum {
     PB_PLAN_SINGLE_TOKEN = 1, /* single_token_attention contract: every query_len == 1 */
     PB_PLAN_FORCE_SIMT = 2,   /* route every span through the SIMT kernel (diagnostics) */
-    PB_PLAN_NO_SPLIT = 4      /* never split a decode span's context across CTAs */
+    PB_PLAN_NO_SPLIT = 4,     /* never split a decode span's context across CTAs */
+    PB_PLAN_SEPARATE_DECODE = 8 /* decode units in their own launch instead of the fused one */
 };
 
 /* Validates the batch exactly as check_batch (src/attention.cpp:23-48, minus the q

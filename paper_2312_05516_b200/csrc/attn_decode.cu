@@ -27,6 +27,8 @@
 #include <math_constants.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 
 namespace pb {
 
@@ -436,6 +438,16 @@ bool decode_supports(int head_size, int chunk, int group) {
 void launch_attn_decode(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens,
                         cudaStream_t stream) {
     if (p.n_items <= 0) return;
+    // GQA groups of 3..16 heads at d = 128 go to the tcgen05 decode kernel (attn_decode_tc.cu);
+    // PB_DECODE=simt keeps them here (profiling comparisons only)
+    static const bool force_simt = [] {
+        const char* e = std::getenv("PB_DECODE");
+        return e && std::string(e) == "simt";
+    }();
+    if (!force_simt && decode_tc_supports(shape.head_size, shape.chunk_size, p.group)) {
+        launch_attn_decode_tc(p, shape, cache, total_tokens, stream);
+        return;
+    }
     sm100_prepare_maps(p, shape, cache, total_tokens);
     const auto* maps = reinterpret_cast<const CUtensorMap*>(cache.maps);
     if (shape.head_size == 128) launch_decode_d<128>(p, maps, stream);

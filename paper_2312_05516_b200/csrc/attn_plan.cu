@@ -36,6 +36,7 @@ struct pb_attn_plan {
     std::vector<WorkItem> tc_items;     // prefill tiles for the sm_100a tcgen05 kernel
     std::vector<WorkItem> decode_items; // single-token split-KV units
     bool decode_kernel = false;         // decode units built (else decode spans go SIMT)
+    bool fused = false;                 // decode units ride in the tile kernel's work list
     cudaStream_t side = nullptr;        // decode units overlap the tile kernel tail
     cudaEvent_t fork = nullptr, join = nullptr;
     int32_t n_groups = 0;
@@ -101,6 +102,7 @@ void validate(const pb_attn_shape& s, int32_t n_spans, const int64_t* qs, const 
 // balance), never more than 64 pages (the decode kernel caches a unit's block-table slice in
 // two registers per lane) and never fewer than 8.
 constexpr int kDecodeUnitsTarget = 4096;
+constexpr int kDecodeUnitsTargetTc = 1536;
 
 void build_work(pb_attn_plan& P) {
     const pb_attn_shape& s = P.shape;
@@ -110,12 +112,18 @@ void build_work(pb_attn_plan& P) {
     // SIMT tiles: blocks of tokens, ~16 rows per warp-pass
     const int simt_tokens = std::max(1, 32 / g);
     const int tc_tokens = tc ? sm100_tile_tokens(g) : 0;
-    P.decode_kernel = tc && decode_supports(s.head_size, s.chunk_size, g);
+    P.decode_kernel = tc && (decode_supports(s.head_size, s.chunk_size, g) ||
+                             decode_tc_supports(s.head_size, s.chunk_size, g));
     std::vector<std::pair<double, WorkItem>> tc_list, dec_list;
     int64_t decode_pages = 0;
     for (const SpanDev& sp : P.spans)
         if (sp.query_len == 1) decode_pages += static_cast<int64_t>(sp.n_pages) * s.n_kv_head;
-    const int split_pages = static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(64, decode_pages / kDecodeUnitsTarget)));
+    // the tcgen05 decode kernel streams one unit per CTA (148 in flight): ~10 units per CTA,
+    // 16..128 pages each; the SIMT kernel streams one unit per warp: ~kDecodeUnitsTarget units
+    const bool dec_tc = P.decode_kernel && decode_tc_supports(s.head_size, s.chunk_size, g);
+    const int split_pages =
+        dec_tc ? static_cast<int>(std::max<int64_t>(16, std::min<int64_t>(128, decode_pages / kDecodeUnitsTargetTc)))
+               : static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(64, decode_pages / kDecodeUnitsTarget)));
     for (int32_t si = 0; si < static_cast<int32_t>(P.spans.size()); ++si) {
         const SpanDev& sp = P.spans[si];
         if (sp.query_len == 0) continue;
@@ -141,7 +149,9 @@ void build_work(pb_attn_plan& P) {
                     w.nt = std::min(tc_tokens, sp.query_len - t0);
                     w.group = -1;
                     const double kv = sp.causal_offset + w.t0 + w.nt;
-                    tc_list.push_back({kv * 4.0, w}); // tensor tile ~ 4x a decode page pass
+                    // est. SM cycles: a 128-position kv tile is ~3400 cycles for two
+                    // query tiles at the measured MMA/softmax rate
+                    tc_list.push_back({kv * (w.nt > tc_tokens / 2 ? 26.5 : 13.3), w});
                     ++P.n_prefill;
                 }
             } else if (!P.decode_kernel) {
@@ -179,17 +189,52 @@ void build_work(pb_attn_plan& P) {
                     w.kv_end = std::min(sp.context_len, (part + 1) * per * s.chunk_size);
                     w.group = group_id;
                     w.part_base = part_base;
-                    dec_list.push_back({static_cast<double>(w.kv_end - w.kv_begin), w});
+                    // est. SM cycles: 8 KB (K+V, d = 128) per 16 positions at 1/148 of HBM
+                    dec_list.push_back({22.5 * static_cast<double>(w.kv_end - w.kv_begin), w});
                     ++P.n_decode;
                 }
             }
         }
     }
+    // One launch for the whole batch: when both kinds exist and the decode units fit the
+    // tensor-core decode path, they join the tile kernel's work list (the fused kernel serves
+    // both; HBM-bound units fill SMs next to tensor-bound tiles).
+    static const bool fuse_all = [] { // profiling: decode-only batches through the fused kernel
+        const char* e = std::getenv("PB_FUSE_DECODE_ONLY");
+        return e && std::atoi(e) != 0;
+    }();
+    P.fused = dec_tc && (!tc_list.empty() || fuse_all) && !dec_list.empty() &&
+              !(P.flags & PB_PLAN_SEPARATE_DECODE);
     // Heavy items first so the persistent CTAs finish together (LPT order).
-    std::stable_sort(tc_list.begin(), tc_list.end(),
-                     [](const auto& a, const auto& b) { return a.first > b.first; });
-    std::stable_sort(dec_list.begin(), dec_list.end(),
-                     [](const auto& a, const auto& b) { return a.first > b.first; });
+    auto lpt = [](auto& v) {
+        std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
+    };
+    lpt(tc_list);
+    lpt(dec_list);
+    if (P.fused) {
+        // Interleave the two LPT lists in proportion to their total cost, so that at every
+        // point of the launch the same share of SMs streams decode pages (HBM) while the rest
+        // run tiles (tensor cores): the decode units then see more than 1/148 of HBM each.
+        double tot[2] = {0, 0}, took[2] = {0, 0};
+        for (auto& e : tc_list) tot[0] += e.first;
+        for (auto& e : dec_list) tot[1] += e.first;
+        std::vector<std::pair<double, WorkItem>> mixed;
+        mixed.reserve(tc_list.size() + dec_list.size());
+        size_t i = 0, k = 0;
+        while (i < tc_list.size() || k < dec_list.size()) {
+            const bool take_tile = k == dec_list.size() ||
+                                   (i < tc_list.size() && took[0] / tot[0] <= took[1] / tot[1]);
+            if (take_tile) {
+                took[0] += tc_list[i].first;
+                mixed.push_back(tc_list[i++]);
+            } else {
+                took[1] += dec_list[k].first;
+                mixed.push_back(dec_list[k++]);
+            }
+        }
+        tc_list.swap(mixed);
+        dec_list.clear();
+    }
     P.tc_items.reserve(tc_list.size());
     for (auto& e : tc_list) P.tc_items.push_back(e.second);
     for (auto& e : dec_list) P.decode_items.push_back(e.second);
@@ -298,7 +343,8 @@ void pb_attn_plan_stats(const pb_attn_plan* P, double* o) {
     o[6] = static_cast<double>(P->simt_items.size());
     double rows = 0;
     for (const auto& w : P->simt_items) rows += static_cast<double>(w.nt) * P->group;
-    for (const auto& w : P->tc_items) rows += static_cast<double>(w.nt) * P->group;
+    for (const auto& w : P->tc_items)
+        if (w.type != kWorkDecode || w.part_idx == 0) rows += static_cast<double>(w.nt) * P->group;
     for (const auto& w : P->decode_items)
         if (w.part_idx == 0) rows += static_cast<double>(w.nt) * P->group;
     o[7] = rows;

@@ -17,7 +17,7 @@ struct Sm100Cache {
     const void* k = nullptr;
     const void* v = nullptr;
     int64_t total_tokens = -1;
-    alignas(64) unsigned char maps[3][128];
+    alignas(64) unsigned char maps[4][128]; // q tiles, k pages, v pages, q decode rows
     bool valid = false;
 };
 
@@ -29,6 +29,9 @@ void sm100_cache_release(Sm100Cache& cache);
 // (re)encodes the q / k / v tensor maps when pointers or sizes changed
 void sm100_prepare_maps(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens);
 bool decode_supports(int head_size, int chunk, int group);
+bool decode_tc_supports(int head_size, int chunk, int group);
+void launch_attn_decode_tc(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache,
+                           int64_t total_tokens, cudaStream_t stream);
 void launch_attn_decode(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens,
                         cudaStream_t stream);
 

@@ -12,7 +12,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:a
   --log-file gpurun_out/${T}_launches_cfg4.csv python bench.py --steps 1 --warmup 3 --layers 8 --no-cpu-baseline > /dev/null 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:attn -c 40 --csv \
   --log-file gpurun_out/${T}_launches_cfg3.csv python bench.py --config 3 --steps 1 --warmup 3 --layers 8 --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_prefill -s 2 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_fused -s 2 -c 1 \
   -o gpurun_out/${T}_prefill python bench.py --steps 1 --warmup 3 --layers 2 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_decode -s 2 -c 1 \
   -o gpurun_out/${T}_decode python bench.py --config 3 --steps 1 --warmup 3 --layers 2 --no-cpu-baseline > /dev/null 2>&1

@@ -12,7 +12,8 @@ for v in ${VARIANTS}; do
   PB_ONLY=${ONLY:-0} PB_LIB=$lib timeout 300 python bench.py --config ${CFG:-4} --steps 5 --warmup 3 --layers 16 --no-cpu-baseline > gpurun_out/${T}_$v.txt 2>&1
 done
 for a in ${EXTRA}; do  # "name:ENV=VAL,ENV2=VAL" bench runs of the product library
-  env ${a#*:} timeout 300 python bench.py --config ${CFG:-4} --steps 5 --warmup 3 --layers 16 --no-cpu-baseline > gpurun_out/${T}_x_${a%%:*}.txt 2>&1
+  kv=${a#*:}
+  env ${kv//,/ } timeout 300 python bench.py --config ${CFG:-4} --steps 5 --warmup 3 --layers 16 --no-cpu-baseline > gpurun_out/${T}_x_${a%%:*}.txt 2>&1
 done
 for a in ${ABLATE}; do
   PB_ABLATE=${a#*:} PB_LIB=${a%%:*} timeout 300 python bench.py --config ${CFG:-4} --steps 5 --warmup 3 --layers 16 --no-cpu-baseline > gpurun_out/${T}_ablate_${a/:/_}.txt 2>&1

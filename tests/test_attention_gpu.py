@@ -233,3 +233,45 @@ def test_bf16_one_shot_equals_device_path(gh):
     dev, _ = gh.run_plan(w, q, k, v)
     host = abi.paged_multi_token_attention(w.shape(), w.batch(), w.host_q(), w.host_pool("k"), w.host_pool("v"))
     assert np.array_equal(host, dev)
+
+
+@pytest.mark.parametrize("n_head,n_kv,all_decode", [(8, 1, False), (8, 2, True), (8, 8, False), (16, 2, False)])
+def test_stale_rows_past_context_cannot_poison(gh, cuda, n_head, n_kv, all_decode):
+    """Rows of a span's last page past its context are never read by the reference
+    (proj/src/attention.cpp:95,119); on the GPU they may hold anything (lazy reclamation,
+    never-written pool memory).  Filling them with NaN must leave every output bit-identical."""
+    torch = cuda
+    rng = SplitMix64(41 + n_head + n_kv)
+    w = random_instance(rng, n_head, n_kv, 128, 16, PB_BF16, 12, 900, all_decode=all_decode, max_q=140)
+    q, k, v = gh.device_inputs(w)
+    base, _ = gh.run_plan(w, q, k, v)
+    assert np.isfinite(base).all()
+    b = w.batch()
+    used = {}  # slot -> rows some span reads
+    for i in range(b.n_spans):
+        ctx = int(b.context_len[i])
+        for pidx, slot in enumerate(b.table(i)):
+            used[int(slot)] = max(used.get(int(slot), 0), min(16, ctx - 16 * pidx))
+    rows = w.row_elems
+    poisoned = 0
+    for slot, n in used.items():
+        if n < 16:
+            a, e = (slot * 16 + n) * rows, (slot + 1) * 16 * rows
+            k[a:e] = float("nan")
+            v[a:e] = float("nan")
+            poisoned += 16 - n
+    assert poisoned > 0
+    after, _ = gh.run_plan(w, q, k, v)
+    assert np.array_equal(after, base)
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_fused_launch_equals_separate_decode_launch(gh, cfg):
+    """The fused launch (decode units in the tile kernel's work list) and the two-launch
+    schedule run the same arithmetic per unit: outputs are bit-identical."""
+    w = config(cfg)
+    q, k, v = gh.device_inputs(w)
+    fused, pf = gh.run_plan(w, q, k, v)
+    sep, ps = gh.run_plan(w, q, k, v, flags=abi.PB_PLAN_SEPARATE_DECODE)
+    assert pf.stats()["decode_units"] == ps.stats()["decode_units"] > 0
+    assert np.array_equal(fused, sep)
