@@ -57,6 +57,10 @@ struct AttnParams {
     float* part_o;           // [n_parts][group][head_size] unnormalised outputs
     int32_t* work_counter;   // persistent-kernel ticket (self-resetting)
     int32_t ablate;          // profiling only (PB_ABLATE): 1 skip softmax math, 2 skip exp
+    // fused launch: decode units next to the tile items (items / n_items)
+    const WorkItem* dec_items;
+    int32_t n_dec_items;
+    int32_t n_dec_ctas;      // CTAs that start on the decode queue
 };
 
 } // namespace pb

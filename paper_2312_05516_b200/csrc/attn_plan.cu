@@ -36,7 +36,8 @@ struct pb_attn_plan {
     std::vector<WorkItem> tc_items;     // prefill tiles for the sm_100a tcgen05 kernel
     std::vector<WorkItem> decode_items; // single-token split-KV units
     bool decode_kernel = false;         // decode units built (else decode spans go SIMT)
-    bool fused = false;                 // decode units ride in the tile kernel's work list
+    bool fused = false;                 // decode units ride in the tile kernel's launch
+    double dec_share = 0;               // fused: est. share of SM time spent on decode units
     cudaStream_t side = nullptr;        // decode units overlap the tile kernel tail
     cudaEvent_t fork = nullptr, join = nullptr;
     int32_t n_groups = 0;
@@ -55,6 +56,17 @@ struct pb_attn_plan {
 namespace {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+int sm_count() {
+    static int n = 0;
+    if (n == 0) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
 
 int dtype_bytes(int dtype) { return dtype == PB_F32 ? 4 : 2; }
 
@@ -212,28 +224,12 @@ void build_work(pb_attn_plan& P) {
     lpt(tc_list);
     lpt(dec_list);
     if (P.fused) {
-        // Interleave the two LPT lists in proportion to their total cost, so that at every
-        // point of the launch the same share of SMs streams decode pages (HBM) while the rest
-        // run tiles (tensor cores): the decode units then see more than 1/148 of HBM each.
-        double tot[2] = {0, 0}, took[2] = {0, 0};
-        for (auto& e : tc_list) tot[0] += e.first;
-        for (auto& e : dec_list) tot[1] += e.first;
-        std::vector<std::pair<double, WorkItem>> mixed;
-        mixed.reserve(tc_list.size() + dec_list.size());
-        size_t i = 0, k = 0;
-        while (i < tc_list.size() || k < dec_list.size()) {
-            const bool take_tile = k == dec_list.size() ||
-                                   (i < tc_list.size() && took[0] / tot[0] <= took[1] / tot[1]);
-            if (take_tile) {
-                took[0] += tc_list[i].first;
-                mixed.push_back(tc_list[i++]);
-            } else {
-                took[1] += dec_list[k].first;
-                mixed.push_back(dec_list[k++]);
-            }
-        }
-        tc_list.swap(mixed);
-        dec_list.clear();
+        // share of the launch's SM time the decode queue needs (est. cycles); the fused kernel
+        // starts that share of its CTAs on decode units, the rest steal once their queue is dry
+        double tot_tile = 0, tot_dec = 0;
+        for (auto& e : tc_list) tot_tile += e.first;
+        for (auto& e : dec_list) tot_dec += e.first;
+        P.dec_share = tot_dec / std::max(1.0, tot_tile + tot_dec);
     }
     P.tc_items.reserve(tc_list.size());
     for (auto& e : tc_list) P.tc_items.push_back(e.second);
@@ -420,6 +416,24 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
         // is forked onto a side stream so its persistent CTAs take SMs as soon as tile CTAs
         // retire (the tile kernel's tail) and the two bottlenecks overlap; joined back before
         // pb_attn_run's stream continues.
+        if (P->fused && only == 0) {
+            // one launch: tile items and decode units from two queues (sm100_attn.cu)
+            static const double cta_scale = [] {
+                const char* e = std::getenv("PB_DEC_CTA_SCALE"); // profiling knob
+                return e ? std::atof(e) : 1.0;
+            }();
+            AttnParams pf = p;
+            pf.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_tc);
+            pf.n_items = static_cast<int32_t>(P->tc_items.size());
+            pf.dec_items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_dec);
+            pf.n_dec_items = static_cast<int32_t>(P->decode_items.size());
+            const int sms = sm_count();
+            const int grid = std::min(sms, pf.n_items + pf.n_dec_items);
+            pf.n_dec_ctas = std::max(1, std::min({grid - 1, pf.n_dec_items,
+                                                  static_cast<int>(std::lround(grid * P->dec_share * cta_scale))}));
+            launch_attn_sm100(pf, P->shape, P->sm100, P->total_tokens, st);
+            return;
+        }
         const bool run_tc = !P->tc_items.empty() && only != 2;
         const bool run_dec = !P->decode_items.empty() && only != 1;
         const bool both = run_tc && run_dec;

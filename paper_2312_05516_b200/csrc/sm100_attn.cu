@@ -25,6 +25,7 @@
 #include "pb_common.hpp"
 #include "sm100_attn.hpp"
 #include "sm100_ptx.cuh"
+#include "decode_tc_cta.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -67,8 +68,6 @@ constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max gr
 
 constexpr int kItemRing = 4; // work items fetched ahead by the TMA warp
 constexpr int kMaxPpt = 16;   // pages per 128-row kv tile (page_tokens >= 8)
-constexpr int kDecN = 16;     // decode units: padded query heads (N of S^T = K Q^T and O^T = V^T P^T)
-constexpr uint32_t kDecPtBytes = 2 * kDecN * 128; // one P^T buffer: [kv half][head][128 B]
 
 template <int D>
 struct __align__(1024) Smem {
@@ -80,13 +79,6 @@ struct __align__(1024) Smem {
     uint64_t s_full[2], p_half[2], p_full[2], o_ready[2], o_empty[2]; // per query tile
     uint64_t item_full[kItemRing], item_empty[kItemRing];   // dynamic tile scheduler ring
     int32_t item_ring[kItemRing];
-    // decode units (fused launch): S^T double buffer, P^T ready, PV done; P^T lives in the
-    // q[1] region, q rows in the q[0] region (decode units do not use query tile B)
-    uint64_t d_s_full[2], d_p_full, d_pv_done;
-    float d_red[2][4][kDecN];
-    float d_redl[4][kDecN];
-    int32_t d_flag;
-    uint32_t tmem_base;
 };
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -108,33 +100,6 @@ __device__ __forceinline__ ItemTiles item_tiles(const WorkItem& w, const SpanDev
     return r;
 }
 
-__device__ __forceinline__ int dec_pages(const WorkItem& w, int chunk) {
-    return (w.kv_end - w.kv_begin + chunk - 1) / chunk;
-}
-__device__ __forceinline__ int dec_tiles(const WorkItem& w, int chunk) {
-    return (dec_pages(w, chunk) * chunk + kTileRows - 1) / kTileRows;
-}
-__device__ __forceinline__ void bar_group0() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
-        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-          "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-}
-__device__ __forceinline__ void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
-    asm volatile(
-        "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-        "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-        "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7]), "r"(r[8]),
-        "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
-        : "memory");
-}
-__device__ __forceinline__ void st_shared_u16(uint32_t addr, uint16_t v) {
-    asm volatile("st.shared.u16 [%0], %1;" ::"r"(addr), "h"(v) : "memory");
-}
-
 // A operand in TMEM (P, bf16), B from shared memory (V).
 __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t b_desc, uint32_t idesc,
                                              uint32_t accumulate) {
@@ -146,6 +111,40 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
         : "memory");
 }
 
+template <int D>
+__device__ __forceinline__ void tile_init(Smem<D>& s) { // thread 0
+    mbar_init(&s.q_full, 1);
+    mbar_init(&s.q_empty, 1);
+    for (int i = 0; i < 2; ++i) {
+        mbar_init(&s.k_full[i], 1);
+        mbar_init(&s.k_empty[i], 1);
+        mbar_init(&s.v_full[i], 1);
+        mbar_init(&s.v_empty[i], 1);
+        mbar_init(&s.s_full[i], 1);
+        mbar_init(&s.p_half[i], 128);
+        mbar_init(&s.p_full[i], 128);
+        mbar_init(&s.o_ready[i], 1);
+        mbar_init(&s.o_empty[i], 128);
+    }
+    for (int i = 0; i < kItemRing; ++i) {
+        mbar_init(&s.item_full[i], 1);
+        mbar_init(&s.item_empty[i], 1 + 8); // MMA thread + the 8 softmax warps
+    }
+}
+template <int D>
+__device__ __forceinline__ void tile_inval(Smem<D>& s) { // thread 0, pipeline drained
+    uint64_t* first = &s.q_full;
+    uint64_t* last = &s.item_empty[kItemRing - 1];
+    for (uint64_t* b = first; b <= last; ++b) mbar_inval(b);
+}
+
+// One launch for the whole ragged batch (BASELINE north star (a)): persistent CTAs, each
+// running the tile pipeline (multi-token spans, tcgen05 QK^T / PV with the GQA group in M)
+// and the decode pipeline (single-token split-KV units, decode_tc_cta.cuh) from two global
+// queues.  CTAs [0, n_dec_ctas) start on decode units and the rest on tile items; a CTA whose
+// queue runs dry drains its pipeline, re-initialises its barriers for the other layout and
+// steals from the other queue, so HBM-bound units stream next to tensor-bound tiles and both
+// queues finish together.
 template <int D, int GD>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fused_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
@@ -155,50 +154,58 @@ __global__ void __launch_bounds__(kThreads, 1)
     constexpr uint32_t kHalfBytes = kTileRows * 128;
     constexpr uint32_t kTileBytes = kTileRows * D * 2;
     extern __shared__ uint8_t smem_raw[];
-    Smem<D>& s = *reinterpret_cast<Smem<D>*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
+    uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    Smem<D>& s = *reinterpret_cast<Smem<D>*>(base);           // tile layout
+    dtc::DtSmem& ds = *reinterpret_cast<dtc::DtSmem*>(base);  // decode layout (same bytes)
+    __shared__ uint32_t tmem_base_sh;
     const int warp = threadIdx.x >> 5;
     const int g = p.group;
     const int tpt = kTileRows / g;         // query tokens per query tile
     const int chunk = p.chunk;
     const int ppt = kTileRows / chunk;     // pages per kv tile
+    int* ctr = p.work_counter;             // [2] next tile item, [3] retired CTAs, [4] next decode unit
 
     if (threadIdx.x == 0) {
-        mbar_init(&s.q_full, 1);
-        mbar_init(&s.q_empty, 1);
-        for (int i = 0; i < 2; ++i) {
-            mbar_init(&s.k_full[i], 1);
-            mbar_init(&s.k_empty[i], 1);
-            mbar_init(&s.v_full[i], 1);
-            mbar_init(&s.v_empty[i], 1);
-            mbar_init(&s.s_full[i], 1);
-            mbar_init(&s.p_half[i], 128);
-            mbar_init(&s.p_full[i], 128);
-            mbar_init(&s.o_ready[i], 1);
-            mbar_init(&s.o_empty[i], 128);
-        }
-        for (int i = 0; i < kItemRing; ++i) {
-            mbar_init(&s.item_full[i], 1);
-            mbar_init(&s.item_empty[i], 1 + 8); // MMA thread + the 8 softmax warps
-        }
-        mbar_init(&s.d_s_full[0], 1);
-        mbar_init(&s.d_s_full[1], 1);
-        mbar_init(&s.d_p_full, 128);
-        mbar_init(&s.d_pv_done, 1);
-        mbar_fence_init();
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
         tma_prefetch(&tm_qd);
     }
-    if (warp == 9) tmem_alloc<kTmemCols>(&s.tmem_base);
+    if (warp == 9) tmem_alloc<kTmemCols>(&tmem_base_sh);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = s.tmem_base;
+    const uint32_t tmem = tmem_base_sh;
     const int wg = warp >> 2;
+    const bool dec_first = static_cast<int>(blockIdx.x) < p.n_dec_ctas;
+    auto mode_items = [&](bool dec) { return dec ? (D == 128 ? p.n_dec_items : 0) : p.n_items; };
+    auto mode_begin = [&](bool dec) {
+        if (threadIdx.x == 0) {
+            if (dec) dtc::decode_cta_init(ds);
+            else tile_init(s);
+            mbar_fence_init();
+        }
+        __syncthreads();
+    };
+    auto mode_end = [&](bool dec) { // pipeline drained: every barrier phase consumed
+        tc_fence_before();
+        __syncthreads();
+        tc_fence_after();
+        if (threadIdx.x == 0) {
+            if (dec) dtc::decode_cta_inval(ds);
+            else tile_inval(s);
+        }
+    };
     if (wg == 2) {
     if (kUseSetMaxNReg) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PB_REG_LO) : "memory");
-    if (warp == 8) {
+    for (int pass = 0; pass < 2; ++pass) {
+    const bool dec = (pass == 0) == dec_first;
+    if (mode_items(dec) == 0) continue;
+    mode_begin(dec);
+    if (dec) {
+        if constexpr (D == 128)
+            dtc::decode_cta_run<GD>(ds, tmem, &tm_qd, &tm_k, &tm_v, p, p.dec_items, p.n_dec_items, ctr + 4, 8, 9, 0);
+    } else if (warp == 8) {
         // ============================ TMA producer ============================
         if (elect_one()) {
             int it = 0, kst = 0, vst = 0;
@@ -208,7 +215,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // Dynamic tile scheduler: the TMA warp takes the next item (items are in LPT order)
             // from a global ticket when it is ready to load it, and hands the index to the MMA
             // and softmax roles through a small shared ring.
-            int* ticket = p.work_counter + 2; // [2] next item, [3] retired CTAs (self-resetting)
+            int* ticket = p.work_counter + 2; // [2] next tile item (reset by the last CTA to retire)
             for (;; ++it) {
                 const int slot = it % kItemRing;
                 if (it >= kItemRing) mbar_wait(&s.item_empty[slot], ((it / kItemRing) - 1) & 1);
@@ -220,29 +227,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const WorkItem w = p.items[item];
                 const SpanDev sp = p.spans[w.span];
                 if (it > 0) mbar_wait(&s.q_empty, (it - 1) & 1);
-                const int32_t* table;
-                int n_pages, n_kv;
-                if (w.type == kWorkDecode) {
-                    // decode unit: the g query rows of one token into the q[0] region, then the
-                    // unit's page range
-                    mbar_arrive_expect_tx(&s.q_full, KH * 128u * static_cast<uint32_t>(g));
-                    for (int h = 0; h < KH; ++h)
-                        tma_load_3d(s.q[0] + h * kHalfBytes, &tm_qd, &s.q_full, h * 64, w.kvh * g, sp.query_start);
-                    table = p.block_tables + sp.bt_off + w.kv_begin / chunk;
-                    n_pages = dec_pages(w, chunk);
-                    n_kv = dec_tiles(w, chunk);
-                } else {
-                    const ItemTiles T = item_tiles(w, sp, tpt);
-                    mbar_arrive_expect_tx(&s.q_full, q_bytes * (T.nt[1] > 0 ? 2u : 1u));
-                    for (int t = 0; t < 2; ++t)
-                        if (T.nt[t] > 0)
-                            for (int h = 0; h < KH; ++h)
-                                tma_load_3d(s.q[t] + h * kHalfBytes, &tm_q, &s.q_full, h * 64, w.kvh * g,
-                                            sp.query_start + w.t0 + t * tpt);
-                    table = p.block_tables + sp.bt_off;
-                    n_pages = sp.n_pages;
-                    n_kv = T.n_kv;
-                }
+                const ItemTiles T = item_tiles(w, sp, tpt);
+                mbar_arrive_expect_tx(&s.q_full, q_bytes * (T.nt[1] > 0 ? 2u : 1u));
+                for (int t = 0; t < 2; ++t)
+                    if (T.nt[t] > 0)
+                        for (int h = 0; h < KH; ++h)
+                            tma_load_3d(s.q[t] + h * kHalfBytes, &tm_q, &s.q_full, h * 64, w.kvh * g,
+                                        sp.query_start + w.t0 + t * tpt);
+                const int32_t* table = p.block_tables + sp.bt_off;
+                const int n_pages = sp.n_pages;
+                const int n_kv = T.n_kv;
                 for (int j = 0; j < n_kv; ++j) {
                     // the tile's block-table entries: independent loads issued together, before
                     // any barrier wait or TMA (one L2 round trip per tile, not one per page)
@@ -272,12 +266,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                 }
             }
-            // the last CTA to retire re-arms the ticket for the next launch
-            __threadfence();
-            if (atomicAdd(ticket + 1, 1) == static_cast<int>(gridDim.x) - 1) {
-                ticket[0] = 0;
-                ticket[1] = 0;
-            }
         }
     } else if (warp == 9) {
         // ============================ MMA issuer =============================
@@ -287,7 +275,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             int it = 0, kst = 0, vst = 0;
             uint32_t kph = 0, vph = 0;
             uint32_t n_p[2] = {0, 0}, n_oe[2] = {0, 0};
-            uint32_t dT = 0; // decode kv tiles issued (S^T buffer / P^T buffer parity)
             for (;; ++it) {
                 const int slot = it % kItemRing;
                 mbar_wait(&s.item_full[slot], (it / kItemRing) & 1);
@@ -295,58 +282,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_arrive(&s.item_empty[slot]);
                 if (item < 0) break;
                 const WorkItem w = p.items[item];
-                if (w.type == kWorkDecode) {
-                    if constexpr (D == 128) {
-                        // S^T = K Q^T (M = 128 kv rows, N = 16 heads) into S_A columns
-                        // [16*(dT&1), +16); O^T += V^T P^T (M = d, N = 16) into O_A
-                        constexpr uint32_t idesc_sd = umma_idesc_bf16(128, kDecN, false, false);
-                        constexpr uint32_t idesc_od = umma_idesc_bf16(128, kDecN, true, false);
-                        const int nt = dec_tiles(w, chunk);
-                        auto issue_sd = [&](uint32_t tile) {
-                            const uint64_t ad = umma_desc_sw128(smem_u32(s.k[kst]), 16, 1024);
-                            const uint64_t bd = umma_desc_sw128(smem_u32(s.q[0]), 16, 1024);
-#pragma unroll
-                            for (int kk = 0; kk < D / 16; ++kk) {
-                                const uint32_t off = ((kk >> 2) * kHalfBytes + (kk & 3) * 32) >> 4;
-                                umma_bf16_ss(tmem + (tile & 1) * kDecN, ad + off, bd + off, idesc_sd, kk > 0);
-                            }
-                            umma_commit(&s.d_s_full[tile & 1]);
-                            umma_commit(&s.k_empty[kst]);
-                            if (++kst == 2) { kst = 0; kph ^= 1; }
-                        };
-                        mbar_wait(&s.q_full, it & 1);
-                        mbar_wait(&s.k_full[kst], kph);
-                        tc_fence_after();
-                        issue_sd(dT);
-                        for (int j = 0; j < nt; ++j, ++dT) {
-                            if (j + 1 < nt) { // S^T(j+1) overlaps softmax(j)
-                                mbar_wait(&s.k_full[kst], kph);
-                                tc_fence_after();
-                                issue_sd(dT + 1);
-                            }
-                            mbar_wait(&s.d_p_full, dT & 1);
-                            if (j == 0) {
-                                mbar_wait(&s.o_empty[0], (n_oe[0] & 1) ^ 1);
-                                ++n_oe[0];
-                            }
-                            mbar_wait(&s.v_full[vst], vph);
-                            tc_fence_after();
-                            const uint64_t ad = umma_desc_sw128(smem_u32(s.v[vst]), kHalfBytes, 1024);
-                            const uint64_t bd = umma_desc_sw128(smem_u32(s.q[1]) + (dT & 1) * kDecPtBytes, 16, 1024);
-#pragma unroll
-                            for (int kk = 0; kk < kTileRows / 16; ++kk) {
-                                const uint32_t ob = ((kk >> 2) * (kDecN * 128) + (kk & 3) * 32) >> 4;
-                                umma_bf16_ss(tmem + kColO, ad + kk * (2048 >> 4), bd + ob, idesc_od,
-                                             (j > 0 || kk > 0) ? 1u : 0u);
-                            }
-                            umma_commit(&s.d_pv_done);
-                            umma_commit(&s.v_empty[vst]);
-                            if (++vst == 2) { vst = 0; vph ^= 1; }
-                        }
-                        umma_commit(&s.q_empty);
-                    }
-                    continue;
-                }
                 const SpanDev sp = p.spans[w.span];
                 const ItemTiles T = item_tiles(w, sp, tpt);
                 mbar_wait(&s.q_full, it & 1);
@@ -419,8 +354,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
         }
     }
+    mode_end(dec);
+    }
     } else {
         if (kUseSetMaxNReg) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(PB_REG_HI) : "memory");
+    for (int pass = 0; pass < 2; ++pass) {
+    const bool dec = (pass == 0) == dec_first;
+    if (mode_items(dec) == 0) continue;
+    mode_begin(dec);
+    if (dec) {
+        if constexpr (D == 128)
+            dtc::decode_cta_run<GD>(ds, tmem, &tm_qd, &tm_k, &tm_v, p, p.dec_items, p.n_dec_items, ctr + 4, 8, 9, 0);
+    } else {
         // ============ softmax / correction / epilogue (one group per query tile) ============
         const int t = wg;                           // query tile of this warpgroup
         const int quad = warp & 3;                  // TMEM lane quadrant of this warp
@@ -432,171 +377,6 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t n_s = 0, n_o = 0;
         uint32_t kv_seen = 0; // kv tiles loaded for earlier items (V ring position)
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
-        uint32_t dT = 0;      // decode kv tiles consumed (group 0 only)
-        // ---- decode unit (group 0): thread `row` owns kv row `row` of each S^T tile and
-        // output dim `row` of O^T (semantics: single_token_attention, attention.cpp:134-188)
-        auto decode_unit = [&](const WorkItem& w, const SpanDev& sp, int nt, uint32_t kvb) {
-            const int lane = threadIdx.x & 31;
-            const uint32_t pt_row = static_cast<uint32_t>((row >> 6) * (kDecN * 128) + (row & 7) * 2);
-            const uint32_t pt_c16 = static_cast<uint32_t>((row & 63) >> 3);
-            float m_run[GD], l_thr[GD];
-#pragma unroll
-            for (int h = 0; h < GD; ++h) {
-                m_run[h] = -CUDART_INF_F;
-                l_thr[h] = 0.f;
-            }
-            for (int j = 0; j < nt; ++j, ++dT) {
-                mbar_wait(&s.d_s_full[dT & 1], (dT >> 1) & 1);
-                tc_fence_after();
-                uint32_t sr[16];
-                tmem_ld16(t_lane + (dT & 1) * kDecN, sr);
-                tmem_ld_wait();
-                const int kv = w.kv_begin + j * kTileRows + row;
-                const bool ok = kv < w.kv_end;
-                float x[GD], mt[GD];
-#pragma unroll
-                for (int h = 0; h < GD; ++h) {
-                    x[h] = (ok && h < g) ? __uint_as_float(sr[h]) * sl2 : -CUDART_INF_F;
-                    float m = x[h];
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-                    mt[h] = m;
-                }
-                if (lane < GD) {
-                    float v = mt[0];
-#pragma unroll
-                    for (int h = 1; h < GD; ++h) v = lane == h ? mt[h] : v;
-                    s.d_red[dT & 1][quad][lane] = v;
-                }
-                bar_group0();
-                bool rescale = false;
-                float corr[GD];
-#pragma unroll
-                for (int h = 0; h < GD; ++h) {
-                    const float m4 = fmaxf(fmaxf(s.d_red[dT & 1][0][h], s.d_red[dT & 1][1][h]),
-                                           fmaxf(s.d_red[dT & 1][2][h], s.d_red[dT & 1][3][h]));
-                    const bool grow = m4 > m_run[h] + kRescaleThreshold; // uniform over the group
-                    const float m_new = grow ? m4 : m_run[h];
-                    corr[h] = grow ? ex2(m_run[h] - m_new) : 1.f;
-                    rescale |= grow && j > 0;
-                    m_run[h] = m_new;
-                }
-                const uint32_t ptb = smem_u32(s.q[1]) + (dT & 1) * kDecPtBytes + pt_row;
-#pragma unroll
-                for (int h = 0; h < GD; ++h) {
-                    if (h < g) {
-                        const float pr = ok ? ex2(x[h] - m_run[h]) : 0.f;
-                        l_thr[h] = l_thr[h] * corr[h] + pr;
-                        const __nv_bfloat16 b = __float2bfloat16_rn(pr);
-                        st_shared_u16(ptb + h * 128 + ((pt_c16 ^ (h & 7)) << 4), *reinterpret_cast<const uint16_t*>(&b));
-                    }
-                }
-                if (!ok && j + 1 == nt) {
-                    // fetched rows past the unit's end may hold anything: zero their V
-                    uint8_t* vrow = s.v[(kvb + j) & 1] + row * 128;
-#pragma unroll
-                    for (int h = 0; h < KH; ++h)
-#pragma unroll
-                        for (int c = 0; c < 8; ++c)
-                            *reinterpret_cast<uint4*>(vrow + h * kHalfBytes + c * 16) = make_uint4(0, 0, 0, 0);
-                }
-                if (j > 0) {
-                    mbar_wait(&s.d_pv_done, (dT - 1) & 1); // PV(j-1) done: O^T may be rescaled
-                    if (rescale) {
-                        tc_fence_after();
-                        uint32_t o[16];
-                        tmem_ld16(t_lane + kColO, o);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int h = 0; h < GD; ++h) o[h] = __float_as_uint(__uint_as_float(o[h]) * corr[h]);
-                        tmem_st16(t_lane + kColO, o);
-                        tmem_st_wait();
-                    }
-                }
-                fence_proxy_async_smem();
-                tc_fence_before();
-                mbar_arrive(&s.d_p_full);
-            }
-            // epilogue: O^T lane `row` = output dim `row`
-            mbar_wait(&s.d_pv_done, (dT - 1) & 1);
-            tc_fence_after();
-            uint32_t o[16];
-            tmem_ld16(t_lane + kColO, o);
-            tmem_ld_wait();
-            tc_fence_before();
-            mbar_arrive(&s.o_empty[0]);
-            float lsum[GD];
-#pragma unroll
-            for (int h = 0; h < GD; ++h) {
-                float v = l_thr[h];
-#pragma unroll
-                for (int off = 16; off > 0; off >>= 1) v += __shfl_xor_sync(0xffffffffu, v, off);
-                lsum[h] = v;
-            }
-            if (lane < GD) {
-                float v = lsum[0];
-#pragma unroll
-                for (int h = 1; h < GD; ++h) v = lane == h ? lsum[h] : v;
-                s.d_redl[quad][lane] = v;
-            }
-            bar_group0();
-            float L[GD];
-#pragma unroll
-            for (int h = 0; h < GD; ++h)
-                L[h] = (s.d_redl[0][h] + s.d_redl[1][h]) + (s.d_redl[2][h] + s.d_redl[3][h]);
-            __nv_bfloat16* orow = out + (static_cast<size_t>(sp.query_start) * p.n_head + static_cast<size_t>(w.kvh) * g) * D;
-            if (w.n_parts <= 1) {
-#pragma unroll
-                for (int h = 0; h < GD; ++h)
-                    if (h < g) orow[static_cast<size_t>(h) * D + row] = __float2bfloat16_rn(__uint_as_float(o[h]) / L[h]);
-                return;
-            }
-            const int part = w.part_base + w.part_idx;
-#pragma unroll
-            for (int h = 0; h < GD; ++h)
-                if (h < g) {
-                    p.part_o[(static_cast<size_t>(part) * g + h) * D + row] = __uint_as_float(o[h]);
-                    if (row == 0) {
-                        p.part_ml[(static_cast<size_t>(part) * g + h) * 2 + 0] = m_run[h];
-                        p.part_ml[(static_cast<size_t>(part) * g + h) * 2 + 1] = L[h];
-                    }
-                }
-            __threadfence();
-            bar_group0();
-            if (row == 0) s.d_flag = atomicAdd(&p.counters[w.group], 1) == w.n_parts - 1;
-            bar_group0();
-            if (!s.d_flag) return;
-            // last split of the group: merge (loads of all heads and 4 parts in flight per step)
-            __threadfence();
-            const int np = w.n_parts;
-            const float* ml = p.part_ml + static_cast<size_t>(w.part_base) * g * 2;
-            const float* po = p.part_o + static_cast<size_t>(w.part_base) * g * D + row;
-            float M[GD], Ls[GD], O[GD];
-#pragma unroll
-            for (int h = 0; h < GD; ++h) {
-                M[h] = -CUDART_INF_F;
-                Ls[h] = 0.f;
-                O[h] = 0.f;
-            }
-#pragma unroll 4
-            for (int q = 0; q < np; ++q)
-#pragma unroll
-                for (int h = 0; h < GD; ++h)
-                    if (h < g) M[h] = fmaxf(M[h], __ldcg(ml + (q * g + h) * 2));
-#pragma unroll 4
-            for (int q = 0; q < np; ++q)
-#pragma unroll
-                for (int h = 0; h < GD; ++h)
-                    if (h < g) {
-                        const float f = ex2(__ldcg(ml + (q * g + h) * 2) - M[h]);
-                        Ls[h] = fmaf(f, __ldcg(ml + (q * g + h) * 2 + 1), Ls[h]);
-                        O[h] = fmaf(f, __ldcg(po + static_cast<size_t>(q * g + h) * D), O[h]);
-                    }
-#pragma unroll
-            for (int h = 0; h < GD; ++h)
-                if (h < g) orow[static_cast<size_t>(h) * D + row] = __float2bfloat16_rn(O[h] / Ls[h]);
-            if (row == 0) p.counters[w.group] = 0; // self-reset for the next launch
-        };
         for (int it = 0;; ++it) {
             const int slot = it % kItemRing;
             mbar_wait(&s.item_full[slot], (it / kItemRing) & 1);
@@ -606,15 +386,6 @@ __global__ void __launch_bounds__(kThreads, 1)
             if (item < 0) break;
             const WorkItem w = p.items[item];
             const SpanDev sp = p.spans[w.span];
-            if (w.type == kWorkDecode) {
-                const int ntd = dec_tiles(w, chunk);
-                const uint32_t kvb = kv_seen;
-                kv_seen += static_cast<uint32_t>(ntd);
-                if constexpr (D == 128) {
-                    if (t == 0) decode_unit(w, sp, ntd, kvb);
-                }
-                continue;
-            }
             const ItemTiles T = item_tiles(w, sp, tpt);
             const int n_tiles = T.ntiles[t];
             const uint32_t kv_base = kv_seen;
@@ -782,8 +553,18 @@ __global__ void __launch_bounds__(kThreads, 1)
             mbar_arrive(&s.o_empty[t]);
         }
     }
-    tc_fence_before();
-    __syncthreads();
+    mode_end(dec);
+    }
+    }
+    // the last CTA to retire re-arms the queues for the next launch
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(ctr + 3, 1) == static_cast<int>(gridDim.x) - 1) {
+            ctr[2] = 0;
+            if (p.n_dec_items > 0) ctr[4] = 0;
+            ctr[3] = 0;
+        }
+    }
     if (warp == 9) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem);
@@ -821,7 +602,7 @@ int g_sms = 0;
 
 template <int D, int GD>
 void launch_fused(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st) {
-    const size_t smem = sizeof(Smem<D>) + 1024;
+    const size_t smem = std::max(sizeof(Smem<D>), sizeof(dtc::DtSmem)) + 1024;
     static bool attr_set = false;
     if (!attr_set) {
         cuda_check(cudaFuncSetAttribute(attn_fused_sm100_kernel<D, GD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -834,7 +615,7 @@ void launch_fused(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st)
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
     }
-    const int grid = std::min(p.n_items, g_sms);
+    const int grid = std::min(p.n_items + (D == 128 ? p.n_dec_items : 0), g_sms);
     attn_fused_sm100_kernel<D, GD><<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
     cuda_check(cudaGetLastError(), "attn_fused_sm100 launch");
     count_launch();
@@ -875,7 +656,7 @@ void sm100_prepare_maps(const AttnParams& p, const pb_attn_shape& shape, Sm100Ca
 
 void launch_attn_sm100(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens,
                        cudaStream_t stream) {
-    if (p.n_items <= 0) return;
+    if (p.n_items + p.n_dec_items <= 0) return;
     sm100_prepare_maps(p, shape, cache, total_tokens);
     const int D = shape.head_size;
     const auto* maps = reinterpret_cast<const CUtensorMap*>(cache.maps);
