@@ -442,10 +442,15 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
                 for (int c = 64; c < 128; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
 #else
+                if (p.ablate == 3) { // profiling: no S read from TMEM (synthetic scores)
 #pragma unroll
-                for (int c = 0; c < 4; ++c)
-                    tmem_ld32(t_lane + col_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
-                tmem_ld_wait();
+                    for (int c = 0; c < 128; ++c) x[c] = __int_as_float((row * 131 + c * 7 + j) & 0x3fffff) * 4.f;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        tmem_ld32(t_lane + col_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
+                    tmem_ld_wait();
+                }
                 // causal mask (only tiles that cross this row's boundary) + running max
                 if (diag) {
 #pragma unroll
