@@ -106,6 +106,18 @@ void pb_attn_plan_stats(const pb_attn_plan* plan, double* out8);
  * (:134-188) on the device. */
 pb_status pb_attn_run(pb_attn_plan* plan, const void* q, const void* k_pages,
                       const void* v_pages, void* out, void* workspace, void* stream);
+/* Layer loop with HOST q / out (the per-layer worker loop of PAPER.md:730-732 when the
+ * projections live on the host side of the boundary): for l < n_layer, q_host[l] is copied
+ * to the device, attended against k_pages[l] / v_pages[l] with the plan, and the result is
+ * copied to out_host[l].  Layer l+1's H2D and layer l-1's D2H run on two copy streams while
+ * layer l computes (two device staging buffers each for q and out, carved from `staging`,
+ * pb_attn_stage_bytes(plan) bytes).  Asynchronous on `stream`: when `stream` completes,
+ * every out_host[l] is written.  Host buffers should be pinned for the copies to overlap. */
+size_t pb_attn_stage_bytes(const pb_attn_plan* plan);
+pb_status pb_attn_run_layers_host(pb_attn_plan* plan, int32_t n_layer, const void* const* q_host,
+                                  void* const* out_host, const void* const* k_pages,
+                                  const void* const* v_pages, void* staging, void* workspace,
+                                  void* stream);
 /* Optional device-side restatement of the reference's NumericError checks: q must be
  * finite (src/attention.cpp:30) and k_row[0] of every attended position must be finite
  * (:100-101).  Writes 0 / PB_ERR_NUMERIC into *d_flag (device int32). */

@@ -129,6 +129,8 @@ _SIGS = {
     "pb_attn_plan_workspace_bytes": (ctypes.c_size_t, [_P]),
     "pb_attn_plan_stats": (None, [_P, _DP]),
     "pb_attn_run": (_I32, [_P, _P, _P, _P, _P, _P, _P]),
+    "pb_attn_stage_bytes": (ctypes.c_size_t, [_P]),
+    "pb_attn_run_layers_host": (_I32, [_P, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "pb_attn_check_numerics": (_I32, [_P, _P, _P, _P, _P]),
     "pb_attn_plan_destroy": (None, [_P]),
     "pb_paged_multi_token_attention": (_I32, [_SHP, _I32, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P]),
@@ -235,6 +237,19 @@ class AttentionPlan:
     def run(self, q: int, k_pages: int, v_pages: int, out: int, workspace: Optional[int],
             stream: Optional[int] = None) -> None:
         check(lib.pb_attn_run(self._h, q, k_pages, v_pages, out, workspace, stream))
+
+    def stage_bytes(self) -> int:
+        return int(lib.pb_attn_stage_bytes(self._h))
+
+    def run_layers_host(self, q_host: Sequence[int], out_host: Sequence[int], k_pages: Sequence[int],
+                        v_pages: Sequence[int], staging: int, workspace: Optional[int],
+                        stream: Optional[int] = None) -> None:
+        """pb_attn_run_layers_host: per-layer host q / out, copies overlapped with compute."""
+        n = len(q_host)
+        arr = ctypes.c_void_p * n
+        self._io_keep = (arr(*q_host), arr(*out_host), arr(*k_pages), arr(*v_pages))
+        check(lib.pb_attn_run_layers_host(self._h, n, *[ctypes.cast(a, _P) for a in self._io_keep], staging,
+                                          workspace, stream))
 
     def check_numerics(self, q: int, k_pages: int, d_flag: int, stream: Optional[int] = None) -> None:
         check(lib.pb_attn_check_numerics(self._h, q, k_pages, d_flag, stream))

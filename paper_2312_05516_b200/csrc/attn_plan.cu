@@ -40,6 +40,8 @@ struct pb_attn_plan {
     double dec_share = 0;               // fused: est. share of SM time spent on decode units
     cudaStream_t side = nullptr;        // decode units overlap the tile kernel tail
     cudaEvent_t fork = nullptr, join = nullptr;
+    cudaStream_t io[2] = {nullptr, nullptr}; // pb_attn_run_layers_host: H2D and D2H streams
+    cudaEvent_t io_ev[10] = {};
     int32_t n_groups = 0;
     int32_t n_parts = 0;
     int32_t n_prefill = 0, n_decode = 0, n_split_spans = 0;
@@ -114,7 +116,7 @@ void validate(const pb_attn_shape& s, int32_t n_spans, const int64_t* qs, const 
 // balance), never more than 64 pages (the decode kernel caches a unit's block-table slice in
 // two registers per lane) and never fewer than 8.
 constexpr int kDecodeUnitsTarget = 4096;
-constexpr int kDecodeUnitsTargetTc = 1536;
+constexpr int kDecodeUnitsTargetTc = 800; // measured: fewer, longer units (fewer merges) stream faster
 
 void build_work(pb_attn_plan& P) {
     const pb_attn_shape& s = P.shape;
@@ -133,8 +135,12 @@ void build_work(pb_attn_plan& P) {
     // the tcgen05 decode kernel streams one unit per CTA (148 in flight): ~10 units per CTA,
     // 16..128 pages each; the SIMT kernel streams one unit per warp: ~kDecodeUnitsTarget units
     const bool dec_tc = P.decode_kernel && decode_tc_supports(s.head_size, s.chunk_size, g);
+    static const int64_t units_tc = [] { // profiling knob: decode units per launch (tcgen05 path)
+        const char* e = std::getenv("PB_DEC_UNITS");
+        return e ? std::max<int64_t>(1, std::atoll(e)) : static_cast<int64_t>(kDecodeUnitsTargetTc);
+    }();
     const int split_pages =
-        dec_tc ? static_cast<int>(std::max<int64_t>(16, std::min<int64_t>(128, decode_pages / kDecodeUnitsTargetTc)))
+        dec_tc ? static_cast<int>(std::max<int64_t>(16, std::min<int64_t>(128, decode_pages / units_tc)))
                : static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(64, decode_pages / kDecodeUnitsTarget)));
     for (int32_t si = 0; si < static_cast<int32_t>(P.spans.size()); ++si) {
         const SpanDev& sp = P.spans[si];
@@ -467,6 +473,60 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
     });
 }
 
+size_t pb_attn_stage_bytes(const pb_attn_plan* P) {
+    if (!P) return 0;
+    const size_t io = align_up(static_cast<size_t>(P->total_tokens) * P->shape.n_head * P->shape.head_size *
+                                   dtype_bytes(P->shape.dtype),
+                               256);
+    return 4 * std::max<size_t>(io, 256); // q[2], out[2]
+}
+
+pb_status pb_attn_run_layers_host(pb_attn_plan* P, int32_t n_layer, const void* const* q_host,
+                                  void* const* out_host, const void* const* k_pages,
+                                  const void* const* v_pages, void* staging, void* workspace,
+                                  void* stream) {
+    return guarded([&] {
+        if (!P) fail(PB_ERR_ERROR, "null plan");
+        if (n_layer < 0) fail(PB_ERR_DIMENSION_MISMATCH, "n_layer < 0");
+        if (n_layer == 0 || P->total_tokens == 0) return;
+        if (!q_host || !out_host || !k_pages || !v_pages || !staging) fail(PB_ERR_ERROR, "null argument");
+        cudaStream_t st = as_stream(stream);
+        if (!P->io[0]) {
+            for (auto& x : P->io) cuda_check(cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking), "io stream");
+            for (auto& e : P->io_ev) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "io event");
+        }
+        cudaStream_t h2d = P->io[0], d2h = P->io[1];
+        // events: [0..1] q ready, [2..3] q free, [4..5] out ready, [6..7] out free
+        cudaEvent_t* ev = P->io_ev;
+        const size_t bytes = static_cast<size_t>(P->total_tokens) * P->shape.n_head * P->shape.head_size *
+                             dtype_bytes(P->shape.dtype);
+        const size_t slot = pb_attn_stage_bytes(P) / 4;
+        auto* base = static_cast<uint8_t*>(staging);
+        // the layer loop starts after whatever is already queued on the caller's stream
+        cuda_check(cudaEventRecord(ev[8], st), "io event");
+        cuda_check(cudaStreamWaitEvent(h2d, ev[8], 0), "io wait");
+        for (int32_t l = 0; l < n_layer; ++l) {
+            const int b = l & 1;
+            void* qd = base + b * slot;
+            void* od = base + (2 + b) * slot;
+            if (l >= 2) cuda_check(cudaStreamWaitEvent(h2d, ev[2 + b], 0), "q free wait");
+            cuda_check(cudaMemcpyAsync(qd, q_host[l], bytes, cudaMemcpyHostToDevice, h2d), "q H2D");
+            cuda_check(cudaEventRecord(ev[b], h2d), "q ready");
+            cuda_check(cudaStreamWaitEvent(st, ev[b], 0), "q ready wait");
+            if (l >= 2) cuda_check(cudaStreamWaitEvent(st, ev[6 + b], 0), "out free wait");
+            const pb_status r = pb_attn_run(P, qd, k_pages[l], v_pages[l], od, workspace, st);
+            if (r != PB_OK) fail(r, "pb_attn_run");
+            cuda_check(cudaEventRecord(ev[2 + b], st), "q free");
+            cuda_check(cudaEventRecord(ev[4 + b], st), "out ready");
+            cuda_check(cudaStreamWaitEvent(d2h, ev[4 + b], 0), "out ready wait");
+            cuda_check(cudaMemcpyAsync(out_host[l], od, bytes, cudaMemcpyDeviceToHost, d2h), "out D2H");
+            cuda_check(cudaEventRecord(ev[6 + b], d2h), "out free");
+        }
+        cuda_check(cudaEventRecord(ev[9], d2h), "io done");
+        cuda_check(cudaStreamWaitEvent(st, ev[9], 0), "io done wait");
+    });
+}
+
 pb_status pb_attn_check_numerics(pb_attn_plan* P, const void* q, const void* k_pages,
                                  int32_t* d_flag, void* stream) {
     return guarded([&] {
@@ -482,6 +542,13 @@ void pb_attn_plan_destroy(pb_attn_plan* P) {
     if (!P) return;
     if (P->d_buf) cudaFree(P->d_buf);
     sm100_cache_release(P->sm100);
+    if (P->io[0]) {
+        for (auto& x : P->io) {
+            cudaStreamSynchronize(x);
+            cudaStreamDestroy(x);
+        }
+        for (auto& e : P->io_ev) cudaEventDestroy(e);
+    }
     if (P->side) {
         cudaStreamSynchronize(P->side);
         cudaStreamDestroy(P->side);

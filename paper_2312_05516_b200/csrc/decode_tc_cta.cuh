@@ -60,6 +60,7 @@ struct __align__(1024) DtSmem {
     uint64_t q_full[2], q_empty[2];
     uint64_t s_full[2], p_full, pv_done, o_empty;
     uint64_t item_full[kRing], item_empty[kRing];
+    uint64_t drain;                 // MMA issuer: every commit of the pass has landed
     int32_t item_ring[kRing];
     uint32_t tmem_base;
 };
@@ -112,6 +113,7 @@ __device__ __forceinline__ void decode_cta_init(DtSmem& s) {
         mbar_init(&s.item_full[i], 1);
         mbar_init(&s.item_empty[i], 1 + 4); // MMA thread + 4 softmax warps
     }
+    mbar_init(&s.drain, 1);
 }
 
 // thread 0 only, pipeline drained: release the barriers' memory for another layout
@@ -132,6 +134,7 @@ __device__ __forceinline__ void decode_cta_inval(DtSmem& s) {
         mbar_inval(&s.item_full[i]);
         mbar_inval(&s.item_empty[i]);
     }
+    mbar_inval(&s.drain);
 }
 
 // One CTA of the decode pipeline.  Roles: warp w_prod = TMA producer, w_mma = MMA issuer,
@@ -219,7 +222,11 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                 mbar_wait(&s.item_full[slot], (it / kRing) & 1);
                 const int item = *reinterpret_cast<volatile int32_t*>(&s.item_ring[slot]);
                 mbar_arrive(&s.item_empty[slot]);
-                if (item < 0) break;
+                if (item < 0) {
+                    umma_commit(&s.drain); // the last commit arrivals land before barriers are reused
+                    mbar_wait(&s.drain, 0);
+                    break;
+                }
                 const WorkItem w = items[item];
                 const int nt = unit_tiles(w, chunk);
                 const int qb = it & 1;

@@ -42,8 +42,10 @@ namespace {
 using namespace pb::sm100;
 
 constexpr int kThreads = 384; // WG0/WG1 softmax of tiles A/B, WG2: TMA warp, MMA warp, 2 spare
-constexpr int kTileRows = 128;        // M rows per query tile and kv rows per kv tile
-constexpr uint32_t kTmemCols = 512;   // S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
+constexpr int kTileRows = 128;        // M rows per query tile
+constexpr int kBN = 64;               // kv rows per kv tile (N of S = Q K^T, K of O += P V)
+constexpr int kKvStages = 3;          // K ring and V ring depth (kBN-row tiles)
+constexpr uint32_t kTmemCols = 512;   // S_A[2] [0,128) S_B[2] [128,256) O_A [256,384) O_B [384,512)
 constexpr uint32_t kColO = 256;
 #ifndef PB_SETMAXNREG
 #define PB_SETMAXNREG 1 // 1: rebalance registers, WG2 (TMA + MMA warps) down, softmax groups up
@@ -59,25 +61,21 @@ constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max gr
 #ifndef PB_POLY_EVERY
 #define PB_POLY_EVERY 0 // one exp2 pair in N on the FMA pipe; 0 = all on MUFU (measured fastest, see profiles/)
 #endif
-#ifndef PB_P_HALF
-#define PB_P_HALF 0     // 1: release P in two halves (measured slower: profiles/r1_variants.md)
-#endif
-#ifndef PB_LD_SPLIT
-#define PB_LD_SPLIT 0   // 1: overlap the second half of the S read with the first half's max
-#endif
 
 constexpr int kItemRing = 4; // work items fetched ahead by the TMA warp
-constexpr int kMaxPpt = 16;   // pages per 128-row kv tile (page_tokens >= 8)
+constexpr int kMaxPpt = kBN / 8; // pages per kv tile (page_tokens >= 8)
 
 template <int D>
 struct __align__(1024) Smem {
-    uint8_t q[2][kTileRows * D * 2];  // tiles A, B: [D/64][128 rows][128 B] K-major SW128
-    uint8_t k[2][kTileRows * D * 2];  // 2-stage ring, same layout
-    uint8_t v[2][kTileRows * D * 2];  // 2-stage ring; read as MN-major SW128 B operand
-    uint64_t q_full, q_empty;
-    uint64_t k_full[2], k_empty[2], v_full[2], v_empty[2];
-    uint64_t s_full[2], p_half[2], p_full[2], o_ready[2], o_empty[2]; // per query tile
+    uint8_t q[2][2][kTileRows * D * 2];   // [item parity][tile A, B]: [D/64][128 rows][128 B] K-major SW128
+    uint8_t k[kKvStages][kBN * D * 2];    // ring of kv tiles: [D/64][64 rows][128 B] K-major SW128
+    uint8_t v[kKvStages][kBN * D * 2];    // same layout, read as the MN-major SW128 B operand
+    uint64_t q_full[2], q_empty[2];       // per item parity (the next item's Q loads early)
+    uint64_t k_full[kKvStages], k_empty[kKvStages], v_full[kKvStages], v_empty[kKvStages];
+    uint64_t s_full[2][2];                // [query tile][S buffer]
+    uint64_t p_full[2], pv_done[2], o_ready[2], o_empty[2]; // per query tile
     uint64_t item_full[kItemRing], item_empty[kItemRing];   // dynamic tile scheduler ring
+    uint64_t drain;                       // MMA issuer: every commit of the pass has landed
     int32_t item_ring[kItemRing];
 };
 
@@ -94,8 +92,8 @@ __device__ __forceinline__ ItemTiles item_tiles(const WorkItem& w, const SpanDev
     ItemTiles r;
     r.nt[0] = min(w.nt, tpt);
     r.nt[1] = w.nt - r.nt[0];
-    r.ntiles[0] = ceil_div(sp.causal_offset + w.t0 + r.nt[0], kTileRows);
-    r.ntiles[1] = r.nt[1] > 0 ? ceil_div(sp.causal_offset + w.t0 + w.nt, kTileRows) : 0;
+    r.ntiles[0] = ceil_div(sp.causal_offset + w.t0 + r.nt[0], kBN);
+    r.ntiles[1] = r.nt[1] > 0 ? ceil_div(sp.causal_offset + w.t0 + w.nt, kBN) : 0;
     r.n_kv = max(r.ntiles[0], r.ntiles[1]);
     return r;
 }
@@ -113,16 +111,21 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
 
 template <int D>
 __device__ __forceinline__ void tile_init(Smem<D>& s) { // thread 0
-    mbar_init(&s.q_full, 1);
-    mbar_init(&s.q_empty, 1);
-    for (int i = 0; i < 2; ++i) {
+    mbar_init(&s.q_full[0], 1);
+    mbar_init(&s.q_full[1], 1);
+    mbar_init(&s.q_empty[0], 1);
+    mbar_init(&s.q_empty[1], 1);
+    for (int i = 0; i < kKvStages; ++i) {
         mbar_init(&s.k_full[i], 1);
         mbar_init(&s.k_empty[i], 1);
         mbar_init(&s.v_full[i], 1);
         mbar_init(&s.v_empty[i], 1);
-        mbar_init(&s.s_full[i], 1);
-        mbar_init(&s.p_half[i], 128);
+    }
+    for (int i = 0; i < 2; ++i) {
+        mbar_init(&s.s_full[i][0], 1);
+        mbar_init(&s.s_full[i][1], 1);
         mbar_init(&s.p_full[i], 128);
+        mbar_init(&s.pv_done[i], 1);
         mbar_init(&s.o_ready[i], 1);
         mbar_init(&s.o_empty[i], 128);
     }
@@ -130,11 +133,12 @@ __device__ __forceinline__ void tile_init(Smem<D>& s) { // thread 0
         mbar_init(&s.item_full[i], 1);
         mbar_init(&s.item_empty[i], 1 + 8); // MMA thread + the 8 softmax warps
     }
+    mbar_init(&s.drain, 1);
 }
 template <int D>
 __device__ __forceinline__ void tile_inval(Smem<D>& s) { // thread 0, pipeline drained
-    uint64_t* first = &s.q_full;
-    uint64_t* last = &s.item_empty[kItemRing - 1];
+    uint64_t* first = &s.q_full[0];
+    uint64_t* last = &s.drain;
     for (uint64_t* b = first; b <= last; ++b) mbar_inval(b);
 }
 
@@ -151,8 +155,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_qd,
                             const AttnParams p) {
     constexpr int KH = D / 64;                  // 64-dim halves (one 128 B swizzle row each)
-    constexpr uint32_t kHalfBytes = kTileRows * 128;
-    constexpr uint32_t kTileBytes = kTileRows * D * 2;
+    constexpr uint32_t kHalfBytes = kTileRows * 128;   // one 64-dim half of a query tile
+    constexpr uint32_t kKvHalf = kBN * 128;            // one 64-dim half of a kv tile
+    constexpr uint32_t kKvTileBytes = kBN * D * 2;
     extern __shared__ uint8_t smem_raw[];
     uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     Smem<D>& s = *reinterpret_cast<Smem<D>*>(base);           // tile layout
@@ -162,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int g = p.group;
     const int tpt = kTileRows / g;         // query tokens per query tile
     const int chunk = p.chunk;
-    const int ppt = kTileRows / chunk;     // pages per kv tile
+    const int ppt = kBN / chunk;           // pages per kv tile
     int* ctr = p.work_counter;             // [2] next tile item, [3] retired CTAs, [4] next decode unit
 
     if (threadIdx.x == 0) {
@@ -226,13 +231,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (item < 0) break;
                 const WorkItem w = p.items[item];
                 const SpanDev sp = p.spans[w.span];
-                if (it > 0) mbar_wait(&s.q_empty, (it - 1) & 1);
+                const int qs = it & 1; // Q buffer set of this item
+                if (it >= 2) mbar_wait(&s.q_empty[qs], ((it >> 1) - 1) & 1);
                 const ItemTiles T = item_tiles(w, sp, tpt);
-                mbar_arrive_expect_tx(&s.q_full, q_bytes * (T.nt[1] > 0 ? 2u : 1u));
+                mbar_arrive_expect_tx(&s.q_full[qs], q_bytes * (T.nt[1] > 0 ? 2u : 1u));
                 for (int t = 0; t < 2; ++t)
                     if (T.nt[t] > 0)
                         for (int h = 0; h < KH; ++h)
-                            tma_load_3d(s.q[t] + h * kHalfBytes, &tm_q, &s.q_full, h * 64, w.kvh * g,
+                            tma_load_3d(s.q[qs][t] + h * kHalfBytes, &tm_q, &s.q_full[qs], h * 64, w.kvh * g,
                                         sp.query_start + w.t0 + t * tpt);
                 const int32_t* table = p.block_tables + sp.bt_off;
                 const int n_pages = sp.n_pages;
@@ -252,16 +258,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uint8_t* dst = which ? s.v[vst] : s.k[kst];
                         const CUtensorMap* tm = which ? &tm_v : &tm_k;
                         mbar_wait(empty, (which ? vph : kph) ^ 1);
-                        mbar_arrive_expect_tx(full, kTileBytes);
+                        mbar_arrive_expect_tx(full, kKvTileBytes);
 #pragma unroll
                         for (int pg = 0; pg < kMaxPpt; ++pg)
                             if (pg < ppt)
                                 for (int h = 0; h < KH; ++h)
-                                    tma_load_3d(dst + h * kHalfBytes + pg * chunk * 128, tm, full, h * 64, w.kvh, rows[pg]);
+                                    tma_load_3d(dst + h * kKvHalf + pg * chunk * 128, tm, full, h * 64, w.kvh, rows[pg]);
                         if (which) {
-                            if (++vst == 2) { vst = 0; vph ^= 1; }
+                            if (++vst == kKvStages) { vst = 0; vph ^= 1; }
                         } else {
-                            if (++kst == 2) { kst = 0; kph ^= 1; }
+                            if (++kst == kKvStages) { kst = 0; kph ^= 1; }
                         }
                     }
                 }
@@ -270,87 +276,81 @@ __global__ void __launch_bounds__(kThreads, 1)
     } else if (warp == 9) {
         // ============================ MMA issuer =============================
         if (elect_one()) {
-            constexpr uint32_t idesc_s = umma_idesc_bf16(128, 128, false, false);
+            constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN, false, false);
             constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
             int it = 0, kst = 0, vst = 0;
             uint32_t kph = 0, vph = 0;
             uint32_t n_p[2] = {0, 0}, n_oe[2] = {0, 0};
+            uint32_t c_s[2] = {0, 0}, c_p[2] = {0, 0}; // per group: S tiles issued / PV tiles issued
             for (;; ++it) {
                 const int slot = it % kItemRing;
                 mbar_wait(&s.item_full[slot], (it / kItemRing) & 1);
                 const int item = *reinterpret_cast<volatile int32_t*>(&s.item_ring[slot]);
                 mbar_arrive(&s.item_empty[slot]);
-                if (item < 0) break;
+                if (item < 0) {
+                    // the pass's last tcgen05.commit arrivals land before its barriers are reused
+                    umma_commit(&s.drain);
+                    mbar_wait(&s.drain, 0);
+                    break;
+                }
                 const WorkItem w = p.items[item];
                 const SpanDev sp = p.spans[w.span];
                 const ItemTiles T = item_tiles(w, sp, tpt);
-                mbar_wait(&s.q_full, it & 1);
+                const int qs = it & 1;
+                mbar_wait(&s.q_full[qs], (it >> 1) & 1);
                 tc_fence_after();
-                // S_t = Q_t K^T for the kv tile in stage kst
-                // descriptors are advanced by adding (byte offset >> 4) to the start-address
-                // field (no carry: shared addresses < 256 KB), which keeps register use low
-                auto issue_s = [&](int t) {
-                    const uint64_t qd = umma_desc_sw128(smem_u32(s.q[t]), 16, 1024);
+                // S_t(jj) = Q_t K(jj)^T into group t's S buffer (c_s[t] & 1), for every group that
+                // needs kv tile jj.  Descriptors are advanced by adding (byte offset >> 4) to the
+                // start-address field (no carry: shared addresses < 256 KB).
+                auto issue_s = [&](int jj) {
+                    mbar_wait(&s.k_full[kst], kph);
+                    tc_fence_after();
                     const uint64_t kd = umma_desc_sw128(smem_u32(s.k[kst]), 16, 1024);
+                    for (int t = 0; t < 2; ++t) {
+                        if (jj >= T.ntiles[t]) continue;
+                        const uint64_t qd = umma_desc_sw128(smem_u32(s.q[qs][t]), 16, 1024);
+                        const uint32_t b = c_s[t] & 1;
 #pragma unroll
-                    for (int kk = 0; kk < D / 16; ++kk) {
-                        const uint32_t off = ((kk >> 2) * kHalfBytes + (kk & 3) * 32) >> 4;
-                        umma_bf16_ss(tmem + t * 128, qd + off, kd + off, idesc_s, kk > 0);
+                        for (int kk = 0; kk < D / 16; ++kk) {
+                            const uint32_t oq = ((kk >> 2) * kHalfBytes + (kk & 3) * 32) >> 4;
+                            const uint32_t ok = ((kk >> 2) * kKvHalf + (kk & 3) * 32) >> 4;
+                            umma_bf16_ss(tmem + t * 128 + b * kBN, qd + oq, kd + ok, idesc_s, kk > 0);
+                        }
+                        umma_commit(&s.s_full[t][b]);
+                        ++c_s[t];
                     }
-                    umma_commit(&s.s_full[t]);
+                    umma_commit(&s.k_empty[kst]);
+                    if (++kst == kKvStages) { kst = 0; kph ^= 1; }
+                    if (jj + 1 == T.n_kv) umma_commit(&s.q_empty[qs]); // Q read by S MMAs only
                 };
-                // S for kv tile 0
-                mbar_wait(&s.k_full[kst], kph);
-                tc_fence_after();
-                for (int t = 0; t < 2; ++t)
-                    if (T.ntiles[t] > 0) issue_s(t);
-                umma_commit(&s.k_empty[kst]);
-                if (++kst == 2) { kst = 0; kph ^= 1; }
+                // S runs one kv tile ahead of PV: S(j+1) is computed while the softmax groups
+                // turn S(j) into P(j) (two S buffers per group)
+                issue_s(0);
                 for (int j = 0; j < T.n_kv; ++j) {
+                    if (j + 1 < T.n_kv) issue_s(j + 1);
                     mbar_wait(&s.v_full[vst], vph);
-                    bool k_next_ready = false;
+                    const uint64_t vd = umma_desc_sw128(smem_u32(s.v[vst]), kKvHalf, 1024);
                     for (int t = 0; t < 2; ++t) {
                         if (j >= T.ntiles[t]) continue;
                         if (j == 0) {
                             mbar_wait(&s.o_empty[t], (n_oe[t] & 1) ^ 1);
                             ++n_oe[t];
                         }
-                        const uint64_t vd = umma_desc_sw128(smem_u32(s.v[vst]), kHalfBytes, 1024);
-                        // kv rows 0..63 as soon as the first half of P_t is in TMEM, then 64..127
-                        mbar_wait(&s.p_half[t], n_p[t] & 1);
-                        tc_fence_after();
-#pragma unroll
-                        for (int kk = 0; kk < kTileRows / 32; ++kk)
-                            umma_bf16_ts(tmem + kColO + t * 128, tmem + t * 128 + kk * 8, vd + kk * (2048 >> 4),
-                                         idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
                         mbar_wait(&s.p_full[t], n_p[t] & 1);
                         ++n_p[t];
                         tc_fence_after();
+                        const uint32_t pcol = t * 128 + (c_p[t] & 1) * kBN; // P (bf16) over S
 #pragma unroll
-                        for (int kk = kTileRows / 32; kk < kTileRows / 16; ++kk)
-                            umma_bf16_ts(tmem + kColO + t * 128, tmem + t * 128 + kk * 8, vd + kk * (2048 >> 4),
-                                         idesc_o, 1u);
+                        for (int kk = 0; kk < kBN / 16; ++kk)
+                            umma_bf16_ts(tmem + kColO + t * 128, tmem + pcol + kk * 8, vd + kk * (2048 >> 4),
+                                         idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+                        ++c_p[t];
+                        umma_commit(&s.pv_done[t]);
                         if (j + 1 == T.ntiles[t]) umma_commit(&s.o_ready[t]);
-                        if (j + 1 < T.ntiles[t]) {
-                            if (!k_next_ready) {
-                                mbar_wait(&s.k_full[kst], kph);
-                                tc_fence_after();
-                                k_next_ready = true;
-                            }
-                            issue_s(t);
-                        }
                     }
                     umma_commit(&s.v_empty[vst]);
-                    if (++vst == 2) { vst = 0; vph ^= 1; }
-                    if (j + 1 < T.n_kv) {
-                        if (!k_next_ready) { // no query tile needed it (cannot happen; keep rings in step)
-                            mbar_wait(&s.k_full[kst], kph);
-                        }
-                        umma_commit(&s.k_empty[kst]);
-                        if (++kst == 2) { kst = 0; kph ^= 1; }
-                    }
+                    if (++vst == kKvStages) { vst = 0; vph ^= 1; }
                 }
-                umma_commit(&s.q_empty);
             }
         }
     }
@@ -371,10 +371,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int quad = warp & 3;                  // TMEM lane quadrant of this warp
         const int row = quad * 32 + (threadIdx.x & 31);
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(quad * 32) << 16);
-        const uint32_t col_s = t * 128;
         const uint32_t col_o = kColO + t * 128;
         const float sl2 = p.scale_log2;
-        uint32_t n_s = 0, n_o = 0;
+        uint32_t n_o = 0;
+        uint32_t c_t = 0;     // kv tiles processed by this group (S buffer / barrier phase)
         uint32_t kv_seen = 0; // kv tiles loaded for earlier items (V ring position)
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
         for (int it = 0;; ++it) {
@@ -401,104 +401,59 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int tok0 = w.t0 + t * tpt;           // first span-relative token of this tile
             const int allowed = sp.causal_offset + tok0 + (valid ? t_local : 0) + 1;
             float m_run = -CUDART_INF_F, l_run = 0.f;
-            for (int j = 0; j < n_tiles; ++j) {
-                mbar_wait(&s.s_full[t], n_s & 1);
-                ++n_s;
+            for (int j = 0; j < n_tiles; ++j, ++c_t) {
+                const uint32_t b = c_t & 1;
+                const uint32_t col_s = t * 128 + b * kBN;
+                mbar_wait(&s.s_full[t][b], (c_t >> 1) & 1);
                 tc_fence_after();
                 if (p.ablate == 1) { // profiling: tensor-core + pipeline bound (P left as S bits)
+                    if (c_t > 0) mbar_wait(&s.pv_done[t], (c_t - 1) & 1);
                     tc_fence_before();
-                    mbar_arrive(&s.p_half[t]);
                     mbar_arrive(&s.p_full[t]);
                     l_run = 1.f;
                     continue;
                 }
-                float x[128];
-                const int kv0 = j * kTileRows;
-                const bool diag = kv0 + kTileRows > allowed;
+                float x[kBN];
+                const int kv0 = j * kBN;
+                const bool diag = kv0 + kBN > allowed;
                 float pm[8];
-#if PB_LD_SPLIT
-                // two halves: the second half's TMEM read is in flight while the first half's
-                // max runs (the wait carries the registers so no use is hoisted above it)
-                tmem_ld32(t_lane + col_s, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
-                tmem_ld32(t_lane + col_s + 32, *reinterpret_cast<uint32_t(*)[32]>(&x[32]));
-                tmem_ld_wait_dep(*reinterpret_cast<uint32_t(*)[32]>(&x[0]));
-                tmem_ld_wait_dep(*reinterpret_cast<uint32_t(*)[32]>(&x[32]));
-                tmem_ld32(t_lane + col_s + 64, *reinterpret_cast<uint32_t(*)[32]>(&x[64]));
-                tmem_ld32(t_lane + col_s + 96, *reinterpret_cast<uint32_t(*)[32]>(&x[96]));
-                if (diag) {
 #pragma unroll
-                    for (int c = 0; c < 64; ++c) x[c] = (kv0 + c < allowed) ? x[c] : -CUDART_INF_F;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; ++u) pm[u] = x[u];
-#pragma unroll
-                for (int c = 8; c < 64; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
-                tmem_ld_wait_dep(*reinterpret_cast<uint32_t(*)[32]>(&x[64]));
-                tmem_ld_wait_dep(*reinterpret_cast<uint32_t(*)[32]>(&x[96]));
-                if (diag) {
-#pragma unroll
-                    for (int c = 64; c < 128; ++c) x[c] = (kv0 + c < allowed) ? x[c] : -CUDART_INF_F;
-                }
-#pragma unroll
-                for (int c = 64; c < 128; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
-#else
-                if (p.ablate == 3) { // profiling: no S read from TMEM (synthetic scores)
-#pragma unroll
-                    for (int c = 0; c < 128; ++c) x[c] = __int_as_float((row * 131 + c * 7 + j) & 0x3fffff) * 4.f;
-                } else {
-#pragma unroll
-                    for (int c = 0; c < 4; ++c)
-                        tmem_ld32(t_lane + col_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
-                    tmem_ld_wait();
-                }
+                for (int c = 0; c < kBN / 32; ++c)
+                    tmem_ld32(t_lane + col_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
+                tmem_ld_wait();
                 // causal mask (only tiles that cross this row's boundary) + running max
                 if (diag) {
 #pragma unroll
-                    for (int c = 0; c < 128; ++c) x[c] = (kv0 + c < allowed) ? x[c] : -CUDART_INF_F;
+                    for (int c = 0; c < kBN; ++c) x[c] = (kv0 + c < allowed) ? x[c] : -CUDART_INF_F;
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) pm[u] = x[u];
 #pragma unroll
-                for (int c = 8; c < 128; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
-#endif
+                for (int c = 8; c < kBN; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
                 const float mt = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
                                        fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * sl2;
                 const bool grow = mt > m_run + kRescaleThreshold;
                 const float m_new = grow ? mt : m_run;
                 const float corr = grow ? ex2(m_run - m_new) : 1.f;
-                // S_t(j) landing implies PV_t(j-1) completed (in-order tensor pipe, the commit for
-                // s_full was issued after it): O_t may be rescaled now, before any of P_t(j) is
-                // released to the tensor core
-                if (j > 0 && __any_sync(0xffffffffu, grow)) {
-#pragma unroll
-                    for (int c = 0; c < D / 32; ++c) {
-                        uint32_t o[32];
-                        tmem_ld32(t_lane + col_o + c * 32, o);
-                        tmem_ld_wait();
-#pragma unroll
-                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-                        tmem_st32(t_lane + col_o + c * 32, o);
-                    }
-                }
-                if (zero_owner && j + 1 == T.n_kv) {
+                if (zero_owner && j + 1 == T.n_kv && row < kBN) {
                     const int kv = kv0 + row;
                     if (kv >= sp.context_len && kv < sp.n_pages * chunk) {
-                        uint8_t* vrow = s.v[(kv_base + j) & 1] + row * 128;
+                        uint8_t* vrow = s.v[(kv_base + j) % kKvStages] + row * 128;
 #pragma unroll
                         for (int h = 0; h < KH; ++h)
 #pragma unroll
                             for (int c = 0; c < 8; ++c)
-                                *reinterpret_cast<uint4*>(vrow + h * kHalfBytes + c * 16) = make_uint4(0, 0, 0, 0);
+                                *reinterpret_cast<uint4*>(vrow + h * kKvHalf + c * 16) = make_uint4(0, 0, 0, 0);
                         fence_proxy_async_smem();
                     }
                 }
                 float2 ps[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) ps[u] = make_float2(0.f, 0.f);
-                uint32_t pk[32];
+                uint32_t pk[kBN / 2];
                 const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_new, -m_new);
 #pragma unroll
-                for (int c = 0; c < 128; c += 2) {
+                for (int c = 0; c < kBN; c += 2) {
                     // exp2((s - max) * log2e / scale) on packed pairs (FFMA2 / FADD2) and MUFU
                     const float2 a = fma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
                     float2 e;
@@ -512,19 +467,29 @@ __global__ void __launch_bounds__(kThreads, 1)
                         e.y = ex2(a.y);
                     }
                     ps[(c >> 1) & 3] = add2(ps[(c >> 1) & 3], e);
-                    pk[(c >> 1) & 31] = pack_bf16x2(e.x, e.y);
-                    if (c == 62 || c == 126) {
-                        // P (bf16) over S_t's columns; with PB_P_HALF the first half is released
-                        // to the tensor core (PV kv rows 0..63) while the second is computed
-                        tmem_st32(t_lane + col_s + (c == 62 ? 0 : 32), pk);
-                        if (PB_P_HALF || c == 126) {
-                            tmem_st_wait();
-                            tc_fence_before();
-                            if (c == 126 && !PB_P_HALF) mbar_arrive(&s.p_half[t]);
-                            mbar_arrive(c == 62 ? &s.p_half[t] : &s.p_full[t]);
-                        }
+                    pk[c >> 1] = pack_bf16x2(e.x, e.y);
+                }
+                // P (bf16) over the first kBN/2 columns of this S buffer
+                tmem_st32(t_lane + col_s, pk);
+                // PV_t of the previous tile must be complete before O_t is rescaled and before
+                // P_t(j) is released; waiting on it every tile also keeps pv_done at most one
+                // phase behind, so its parity wait is exact
+                if (c_t > 0) mbar_wait(&s.pv_done[t], (c_t - 1) & 1);
+                if (j > 0 && __any_sync(0xffffffffu, grow)) {
+                    tc_fence_after();
+#pragma unroll
+                    for (int c = 0; c < D / 32; ++c) {
+                        uint32_t o[32];
+                        tmem_ld32(t_lane + col_o + c * 32, o);
+                        tmem_ld_wait();
+#pragma unroll
+                        for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
+                        tmem_st32(t_lane + col_o + c * 32, o);
                     }
                 }
+                tmem_st_wait();
+                tc_fence_before();
+                mbar_arrive(&s.p_full[t]);
                 const float2 s2 = add2(add2(ps[0], ps[1]), add2(ps[2], ps[3]));
                 const float sum = s2.x + s2.y;
                 l_run = l_run * corr + sum;
@@ -629,7 +594,7 @@ void launch_fused(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st)
 } // namespace
 
 bool sm100_supports(int head_size, int chunk, int group) {
-    return (head_size == 64 || head_size == 128) && chunk >= 8 && chunk <= 128 && (128 % chunk) == 0 &&
+    return (head_size == 64 || head_size == 128) && chunk >= 8 && chunk <= kBN && (kBN % chunk) == 0 &&
            group >= 1 && group <= 128;
 }
 

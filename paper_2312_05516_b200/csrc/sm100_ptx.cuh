@@ -7,6 +7,7 @@
 
 #include <cuda.h>
 #include <cstdint>
+#include <cstdio>
 
 namespace pb::sm100 {
 
@@ -44,8 +45,21 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     const uint32_t a = smem_u32(bar);
+#ifdef PB_WATCHDOG
+    // debugging builds only: a wait that lasts ~2 s reports the barrier and traps, so a
+    // pipeline bug ends the launch with an error instead of hanging the GPU
+    const long long t0 = clock64();
+    while (!mbar_try_wait(a, parity)) {
+        if (clock64() - t0 > 4000000000LL) {
+            printf("PB_WATCHDOG: block %d thread %d stuck on smem barrier 0x%x parity %u\n", blockIdx.x,
+                   threadIdx.x, a, parity);
+            __trap();
+        }
+    }
+#else
     while (!mbar_try_wait(a, parity)) {
     }
+#endif
 }
 
 // ---------------------------------------------------------------- fences

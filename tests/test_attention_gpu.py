@@ -275,3 +275,33 @@ def test_fused_launch_equals_separate_decode_launch(gh, cfg):
     sep, ps = gh.run_plan(w, q, k, v, flags=abi.PB_PLAN_SEPARATE_DECODE)
     assert pf.stats()["decode_units"] == ps.stats()["decode_units"] > 0
     assert np.array_equal(fused, sep)
+
+
+def test_layers_host_pipeline_matches_per_layer_runs(gh, cuda):
+    """pb_attn_run_layers_host (host q / out, copies overlapped with compute) gives the same
+    bits as one pb_attn_run per layer on device buffers."""
+    torch = cuda
+    rng = SplitMix64(77)
+    w = random_instance(rng, 16, 2, 128, 16, PB_BF16, 6, 900, max_q=120)
+    n_layer = 3
+    qs, ks, vs = [], [], []
+    for l in range(n_layer):
+        q, k, v = gh.device_inputs(w, layer=l)
+        qs.append(q * (1.0 + 0.25 * l))  # a different q per layer
+        ks.append(k)
+        vs.append(v)
+    want = [gh.run_plan(w, qs[l], ks[l], vs[l])[0] for l in range(n_layer)]
+    plan = AttentionPlan(w.shape(), w.batch())
+    stream = torch.cuda.current_stream().cuda_stream
+    plan.upload(stream)
+    ws = torch.zeros(max(1, plan.workspace_bytes()), dtype=torch.uint8, device="cuda")
+    stage = torch.empty(plan.stage_bytes(), dtype=torch.uint8, device="cuda")
+    q_host = [q.cpu().pin_memory() for q in qs]
+    out_host = [torch.empty_like(q_host[0]).pin_memory() for _ in range(n_layer)]
+    plan.run_layers_host([t.data_ptr() for t in q_host], [t.data_ptr() for t in out_host],
+                         [t.data_ptr() for t in ks], [t.data_ptr() for t in vs], stage.data_ptr(),
+                         ws.data_ptr(), stream)
+    torch.cuda.synchronize()
+    n = w.total_tokens * w.n_head * w.head_size
+    for l in range(n_layer):
+        assert np.array_equal(out_host[l].float().numpy()[:n], want[l])
