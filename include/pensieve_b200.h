@@ -114,6 +114,9 @@ pb_status pb_attn_run(pb_attn_plan* plan, const void* q, const void* k_pages,
  * pb_attn_stage_bytes(plan) bytes).  Asynchronous on `stream`: when `stream` completes,
  * every out_host[l] is written.  Host buffers should be pinned for the copies to overlap. */
 size_t pb_attn_stage_bytes(const pb_attn_plan* plan);
+/* Diagnostics: when d_trace (device, >= 148 * 2 * 4 uint64) is set, the fused launch writes
+ * per CTA and pass {mode (0 tile, 1 decode), items taken, begin ns, end ns}.  NULL disables. */
+void pb_attn_set_trace(pb_attn_plan* plan, void* d_trace);
 pb_status pb_attn_run_layers_host(pb_attn_plan* plan, int32_t n_layer, const void* const* q_host,
                                   void* const* out_host, const void* const* k_pages,
                                   const void* const* v_pages, void* staging, void* workspace,

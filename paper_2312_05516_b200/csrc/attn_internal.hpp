@@ -61,6 +61,9 @@ struct AttnParams {
     const WorkItem* dec_items;
     int32_t n_dec_items;
     int32_t n_dec_ctas;      // CTAs that start on the decode queue
+    // diagnostics only (pb_attn_set_trace): per CTA and pass, {mode, items, t_begin, t_end}
+    // in %globaltimer ns, 4 x uint64 per (CTA, pass); null in production
+    unsigned long long* trace;
 };
 
 } // namespace pb

@@ -38,6 +38,7 @@ struct pb_attn_plan {
     bool decode_kernel = false;         // decode units built (else decode spans go SIMT)
     bool fused = false;                 // decode units ride in the tile kernel's launch
     double dec_share = 0;               // fused: est. share of SM time spent on decode units
+    void* trace = nullptr;              // diagnostics: per-CTA pass timeline (pb_attn_set_trace)
     cudaStream_t side = nullptr;        // decode units overlap the tile kernel tail
     cudaEvent_t fork = nullptr, join = nullptr;
     cudaStream_t io[2] = {nullptr, nullptr}; // pb_attn_run_layers_host: H2D and D2H streams
@@ -401,6 +402,7 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
             return e ? std::atoi(e) : 0;
         }();
         p.ablate = ablate;
+        p.trace = static_cast<unsigned long long*>(P->trace);
         // profiling only (PB_ONLY): 1 = run only the tile kernel, 2 = only the decode kernel
         static const int only = [] {
             const char* e = std::getenv("PB_ONLY");
@@ -471,6 +473,10 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
             cuda_check(cudaStreamWaitEvent(st, P->join, 0), "join wait");
         }
     });
+}
+
+void pb_attn_set_trace(pb_attn_plan* P, void* d_trace) {
+    if (P) P->trace = d_trace;
 }
 
 size_t pb_attn_stage_bytes(const pb_attn_plan* P) {

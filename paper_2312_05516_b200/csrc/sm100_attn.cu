@@ -184,7 +184,17 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int wg = warp >> 2;
     const bool dec_first = static_cast<int>(blockIdx.x) < p.n_dec_ctas;
     auto mode_items = [&](bool dec) { return dec ? (D == 128 ? p.n_dec_items : 0) : p.n_items; };
+    auto gtime = []() {
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        return t;
+    };
     auto mode_begin = [&](bool dec) {
+        if (threadIdx.x == 0 && p.trace) {
+            unsigned long long* tr = p.trace + (static_cast<size_t>(blockIdx.x) * 2 + (dec == dec_first ? 0 : 1)) * 4;
+            tr[0] = dec ? 1 : 0;
+            tr[2] = gtime();
+        }
         if (threadIdx.x == 0) {
             if (dec) dtc::decode_cta_init(ds);
             else tile_init(s);
@@ -199,6 +209,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (threadIdx.x == 0) {
             if (dec) dtc::decode_cta_inval(ds);
             else tile_inval(s);
+            if (p.trace)
+                p.trace[(static_cast<size_t>(blockIdx.x) * 2 + (dec == dec_first ? 0 : 1)) * 4 + 3] = gtime();
         }
     };
     if (wg == 2) {
