@@ -106,6 +106,14 @@ void pb_attn_plan_stats(const pb_attn_plan* plan, double* out8);
  * (:134-188) on the device. */
 pb_status pb_attn_run(pb_attn_plan* plan, const void* q, const void* k_pages,
                       const void* v_pages, void* out, void* workspace, void* stream);
+/* pb_attn_run with the paged K/V append fused in (the row-write loop of
+ * qkv_project, src/attention.cpp:315-327): k_new / v_new hold the batch's new K/V rows
+ * [total_tokens][n_kv_head][head_size] in query order; token i of span s is written to
+ * position causal_offset[s] + i (page block_table[pos / chunk], row pos % chunk) before any
+ * attention reads it.  Equivalent to pb_kv_append followed by pb_attn_run, in one launch on
+ * the tcgen05 paths (a grid-wide barrier separates the writes from the reads). */
+pb_status pb_attn_run_append(pb_attn_plan* plan, const void* q, const void* k_new, const void* v_new,
+                             void* k_pages, void* v_pages, void* out, void* workspace, void* stream);
 /* Layer loop with HOST q / out (the per-layer worker loop of PAPER.md:730-732 when the
  * projections live on the host side of the boundary): for l < n_layer, q_host[l] is copied
  * to the device, attended against k_pages[l] / v_pages[l] with the plan, and the result is

@@ -130,6 +130,7 @@ _SIGS = {
     "pb_attn_plan_stats": (None, [_P, _DP]),
     "pb_attn_run": (_I32, [_P, _P, _P, _P, _P, _P, _P]),
     "pb_attn_stage_bytes": (ctypes.c_size_t, [_P]),
+    "pb_attn_run_append": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "pb_attn_set_trace": (None, [_P, _P]),
     "pb_attn_run_layers_host": (_I32, [_P, _I32, _P, _P, _P, _P, _P, _P, _P]),
     "pb_attn_check_numerics": (_I32, [_P, _P, _P, _P, _P]),
@@ -238,6 +239,11 @@ class AttentionPlan:
     def run(self, q: int, k_pages: int, v_pages: int, out: int, workspace: Optional[int],
             stream: Optional[int] = None) -> None:
         check(lib.pb_attn_run(self._h, q, k_pages, v_pages, out, workspace, stream))
+
+    def run_append(self, q: int, k_new: int, v_new: int, k_pages: int, v_pages: int, out: int,
+                   workspace: Optional[int], stream: Optional[int] = None) -> None:
+        """pb_attn_run_append: write the batch's new K/V rows into the pages, then attend."""
+        check(lib.pb_attn_run_append(self._h, q, k_new, v_new, k_pages, v_pages, out, workspace, stream))
 
     def set_trace(self, d_trace: Optional[int]) -> None:
         lib.pb_attn_set_trace(self._h, d_trace)

@@ -2,6 +2,7 @@
 // batches, or PB_PLAN_SEPARATE_DECODE).  The pipeline itself is decode_tc_cta.cuh, shared with
 // the fused launch (sm100_attn.cu).
 #include "decode_tc_cta.cuh"
+#include "append_prologue.cuh"
 #include "pb_common.hpp"
 #include "sm100_attn.hpp"
 
@@ -21,6 +22,7 @@ __global__ void __launch_bounds__(kDtThreads, 1)
     extern __shared__ uint8_t smem_raw[];
     DtSmem& s = *reinterpret_cast<DtSmem*>(smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u));
     const int warp = threadIdx.x >> 5;
+    append_prologue(p, p.work_counter); // fused K/V append, when the launch carries new rows
     if (threadIdx.x == 0) {
         decode_cta_init(s);
         mbar_fence_init();
@@ -50,6 +52,11 @@ __global__ void __launch_bounds__(kDtThreads, 1)
     }
 }
 
+__global__ void __launch_bounds__(256) append_spans_kernel(const AttnParams p) {
+    append_rows(p, static_cast<int>((blockIdx.x * blockDim.x + threadIdx.x) >> 5),
+                static_cast<int>((gridDim.x * blockDim.x) >> 5));
+}
+
 int g_dt_sms = 0;
 
 template <int G>
@@ -74,6 +81,14 @@ void launch_dt(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st) {
 }
 
 } // namespace
+
+void launch_append_spans(const AttnParams& p, cudaStream_t stream) {
+    if (!p.k_new || p.total_tokens <= 0) return;
+    const int grid = std::max(1, std::min(1184, (p.total_tokens + 7) / 8));
+    append_spans_kernel<<<grid, 256, 0, stream>>>(p);
+    cuda_check(cudaGetLastError(), "append launch");
+    count_launch();
+}
 
 bool decode_tc_supports(int head_size, int chunk, int group) {
     return head_size == 128 && chunk >= 8 && chunk <= 128 && (128 % chunk) == 0 && group >= 1 && group <= kN;

@@ -64,6 +64,12 @@ struct AttnParams {
     // diagnostics only (pb_attn_set_trace): per CTA and pass, {mode, items, t_begin, t_end}
     // in %globaltimer ns, 4 x uint64 per (CTA, pass); null in production
     unsigned long long* trace;
+    // fused K/V append (pb_attn_run_append): new rows [total_tokens][n_kv][d], null = none
+    const void* k_new;
+    const void* v_new;
+    int32_t total_tokens;
+    int32_t n_spans;
+    int32_t row_bytes;       // n_kv_head * head_size * element bytes
 };
 
 } // namespace pb

@@ -365,6 +365,9 @@ static AttnParams make_params(pb_attn_plan* P, const void* q, const void* k, con
     p.scale = static_cast<float>(P->shape.scale);
     p.scale_log2 = static_cast<float>(1.4426950408889634 / P->shape.scale);
     p.n_groups = P->n_groups;
+    p.total_tokens = static_cast<int32_t>(P->total_tokens);
+    p.n_spans = static_cast<int32_t>(P->spans.size());
+    p.row_bytes = P->shape.n_kv_head * P->shape.head_size * dtype_bytes(P->shape.dtype);
     auto* base = static_cast<uint8_t*>(P->d_buf);
     p.spans = reinterpret_cast<const SpanDev*>(base);
     p.block_tables = reinterpret_cast<const int32_t*>(base + P->off_bt);
@@ -386,9 +389,11 @@ static AttnParams make_params(pb_attn_plan* P, const void* q, const void* k, con
     return p;
 }
 
-pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const void* v_pages,
-                      void* out, void* workspace, void* stream) {
-    return guarded([&] {
+// One attention launch sequence for a layer; with k_new / v_new the batch's new K/V rows are
+// first written into the pages (fused into the launch where possible).
+static void run_impl(pb_attn_plan* P, const void* q, const void* k_pages, const void* v_pages, void* out,
+                     void* workspace, void* stream, const void* k_new, const void* v_new) {
+
         if (!P) fail(PB_ERR_ERROR, "null plan");
         if (!P->uploaded) fail(PB_ERR_ERROR, "plan not uploaded (call pb_attn_plan_upload)");
         if (P->total_tokens == 0) return;
@@ -413,6 +418,23 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
             cuda_check(cudaMemsetAsync(workspace, 0, 256 + align_up(sizeof(int32_t) * P->n_groups, 256), st),
                        "workspace init");
             P->last_workspace = workspace;
+        }
+        if (k_new) {
+            // fused append: inside the (single) attention launch when there is one, else a
+            // stand-alone row-write launch first (the same rows, the same addressing)
+            const bool single = only == 0 && P->simt_items.empty() && P->shape.dtype == PB_BF16 &&
+                                (P->fused || P->decode_items.empty() ||
+                                 (P->tc_items.empty() && decode_tc_supports(P->shape.head_size, P->shape.chunk_size,
+                                                                            P->group)));
+            if (single) {
+                p.k_new = k_new;
+                p.v_new = v_new;
+            } else {
+                AttnParams pa = p;
+                pa.k_new = k_new;
+                pa.v_new = v_new;
+                launch_append_spans(pa, st);
+            }
         }
         if (!P->simt_items.empty()) {
             AttnParams ps = p;
@@ -472,6 +494,18 @@ pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const
             cuda_check(cudaEventRecord(P->join, P->side), "join");
             cuda_check(cudaStreamWaitEvent(st, P->join, 0), "join wait");
         }
+    }
+
+pb_status pb_attn_run(pb_attn_plan* P, const void* q, const void* k_pages, const void* v_pages,
+                      void* out, void* workspace, void* stream) {
+    return guarded([&] { run_impl(P, q, k_pages, v_pages, out, workspace, stream, nullptr, nullptr); });
+}
+
+pb_status pb_attn_run_append(pb_attn_plan* P, const void* q, const void* k_new, const void* v_new,
+                             void* k_pages, void* v_pages, void* out, void* workspace, void* stream) {
+    return guarded([&] {
+        if (!k_new || !v_new) fail(PB_ERR_ERROR, "null new-row pointer");
+        run_impl(P, q, k_pages, v_pages, out, workspace, stream, k_new, v_new);
     });
 }
 

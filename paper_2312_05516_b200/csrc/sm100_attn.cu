@@ -26,6 +26,7 @@
 #include "sm100_attn.hpp"
 #include "sm100_ptx.cuh"
 #include "decode_tc_cta.cuh"
+#include "append_prologue.cuh"
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -170,6 +171,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ppt = kBN / chunk;           // pages per kv tile
     int* ctr = p.work_counter;             // [2] next tile item, [3] retired CTAs, [4] next decode unit
 
+    append_prologue(p, ctr); // fused K/V append, when the launch carries new rows
     if (threadIdx.x == 0) {
         tma_prefetch(&tm_q);
         tma_prefetch(&tm_k);

@@ -30,6 +30,8 @@ void sm100_cache_release(Sm100Cache& cache);
 void sm100_prepare_maps(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens);
 bool decode_supports(int head_size, int chunk, int group);
 bool decode_tc_supports(int head_size, int chunk, int group);
+// stand-alone launch of the fused append's row writes (bf16 rows; paths without the prologue)
+void launch_append_spans(const AttnParams& p, cudaStream_t stream);
 void launch_attn_decode_tc(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache,
                            int64_t total_tokens, cudaStream_t stream);
 void launch_attn_decode(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens,

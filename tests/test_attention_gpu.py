@@ -305,3 +305,62 @@ def test_layers_host_pipeline_matches_per_layer_runs(gh, cuda):
     n = w.total_tokens * w.n_head * w.head_size
     for l in range(n_layer):
         assert np.array_equal(out_host[l].float().numpy()[:n], want[l])
+
+
+def _append_reference(torch, w, k_new, v_new, k_pages, v_pages):
+    """pb_kv_append (the stand-alone qkv_project write loop) for the batch's new tokens."""
+    b = w.batch()
+    shape = w.shape()
+    n_rows = np.ascontiguousarray(b.query_len, dtype=np.int64)
+    row_start = np.ascontiguousarray(np.concatenate([[0], np.cumsum(n_rows)[:-1]]), dtype=np.int64)
+    start = np.ascontiguousarray(b.causal_offset, dtype=np.int64)
+    bt = np.ascontiguousarray(b.bt, dtype=np.int32)
+    bt_off = np.ascontiguousarray(b.bt_off, dtype=np.int64)
+    dev = [torch.from_numpy(a).cuda() for a in (row_start, n_rows, start, bt, bt_off)]
+    p = lambda a: a.ctypes.data  # noqa: E731
+    abi.check(abi.lib.pb_kv_append(abi.ctypes.byref(shape), b.n_spans, p(row_start), p(n_rows), p(start), p(bt),
+                                   p(bt_off), *[d.data_ptr() for d in dev], k_new.data_ptr(), v_new.data_ptr(),
+                                   k_pages.data_ptr(), v_pages.data_ptr(), None))
+
+
+@pytest.mark.parametrize("case", ["fused_gqa8", "decode_only", "prefill_only", "d64_fallback", "fp32_fallback"])
+def test_fused_append_equals_append_then_attention(gh, cuda, case):
+    """pb_attn_run_append (new K/V rows written inside the attention launch, grid barrier
+    before any page read) == pb_kv_append + pb_attn_run: same pages, same outputs, bit for bit."""
+    torch = cuda
+    rng = SplitMix64(300 + len(case))
+    if case == "fused_gqa8":
+        w = random_instance(rng, 16, 2, 128, 16, PB_BF16, 40, 1500, max_q=200)
+    elif case == "decode_only":
+        w = random_instance(rng, 16, 2, 128, 16, PB_BF16, 60, 2000, all_decode=True)
+    elif case == "prefill_only":
+        w = random_instance(rng, 8, 8, 128, 16, PB_BF16, 5, 600, max_q=600)
+        b = w.batch()
+        assert min(b.query_len) >= 1
+    elif case == "d64_fallback":
+        w = random_instance(rng, 8, 2, 64, 16, PB_BF16, 12, 700, max_q=90)
+    else:
+        w = random_instance(rng, 8, 2, 64, 16, PB_F32, 6, 300, max_q=40)
+    q, k, v = gh.device_inputs(w)
+    dt = q.dtype
+    row = w.n_kv_head * w.head_size
+    k_new = torch.empty(w.total_tokens * row, dtype=dt, device="cuda")
+    v_new = torch.empty_like(k_new)
+    abi.fill_unit(k_new.data_ptr(), w.dtype, k_new.numel(), 991, 0)
+    abi.fill_unit(v_new.data_ptr(), w.dtype, v_new.numel(), 992, 0)
+    k1, v1 = k.clone(), v.clone()
+    _append_reference(torch, w, k_new, v_new, k1, v1)
+    want, _ = gh.run_plan(w, q, k1, v1)
+    plan = AttentionPlan(w.shape(), w.batch())
+    stream = torch.cuda.current_stream().cuda_stream
+    plan.upload(stream)
+    out = torch.zeros_like(q)
+    ws = torch.zeros(max(1, plan.workspace_bytes()), dtype=torch.uint8, device="cuda")
+    k2, v2 = k.clone(), v.clone()
+    for _ in range(2):  # the grid barrier re-arms itself across launches
+        plan.run_append(q.data_ptr(), k_new.data_ptr(), v_new.data_ptr(), k2.data_ptr(), v2.data_ptr(),
+                        out.data_ptr(), ws.data_ptr(), stream)
+    torch.cuda.synchronize()
+    assert torch.equal(k1, k2) and torch.equal(v1, v2)
+    n = w.total_tokens * w.n_head * w.head_size
+    assert np.array_equal(out.float().cpu().numpy()[:n], want)
