@@ -39,6 +39,9 @@ struct pb_attn_plan {
     bool fused = false;                 // decode units ride in the tile kernel's launch
     double dec_share = 0;               // fused: est. share of SM time spent on decode units
     void* trace = nullptr;              // diagnostics: per-CTA pass timeline (pb_attn_set_trace)
+    void* h_buf = nullptr;              // pinned upload staging
+    size_t h_bytes = 0;
+    cudaEvent_t up_done = nullptr;
     cudaStream_t side = nullptr;        // decode units overlap the tile kernel tail
     cudaEvent_t fork = nullptr, join = nullptr;
     cudaStream_t io[2] = {nullptr, nullptr}; // pb_attn_run_layers_host: H2D and D2H streams
@@ -308,19 +311,31 @@ pb_status pb_attn_plan_upload(pb_attn_plan* P, void* stream) {
             cuda_check(cudaMalloc(&P->d_buf, total), "cudaMalloc(plan descriptors)");
             P->d_bytes = total;
         }
-        // One pinned staging copy so the H2D is a single async transfer.
-        std::vector<uint8_t> host(total, 0);
-        if (b_spans) std::memcpy(host.data(), P->spans.data(), b_spans);
-        if (!P->bt.empty()) std::memcpy(host.data() + P->off_bt, P->bt.data(), sizeof(int32_t) * P->bt.size());
+        // One pinned staging copy so the H2D is a single transfer that does not block the
+        // host; the staging buffer is reused only after its previous upload completed.
+        if (P->h_bytes < total) {
+            if (P->h_buf) {
+                cudaEventSynchronize(P->up_done);
+                cudaFreeHost(P->h_buf);
+            }
+            P->h_buf = nullptr;
+            cuda_check(cudaMallocHost(&P->h_buf, total), "cudaMallocHost(plan staging)");
+            P->h_bytes = total;
+        }
+        if (!P->up_done) cuda_check(cudaEventCreateWithFlags(&P->up_done, cudaEventDisableTiming), "event");
+        else cuda_check(cudaEventSynchronize(P->up_done), "plan staging reuse");
+        auto* host = static_cast<uint8_t*>(P->h_buf);
+        std::memset(host, 0, total);
+        if (b_spans) std::memcpy(host, P->spans.data(), b_spans);
+        if (!P->bt.empty()) std::memcpy(host + P->off_bt, P->bt.data(), sizeof(int32_t) * P->bt.size());
         if (!P->simt_items.empty())
-            std::memcpy(host.data() + P->off_simt, P->simt_items.data(), sizeof(WorkItem) * P->simt_items.size());
+            std::memcpy(host + P->off_simt, P->simt_items.data(), sizeof(WorkItem) * P->simt_items.size());
         if (!P->tc_items.empty())
-            std::memcpy(host.data() + P->off_tc, P->tc_items.data(), sizeof(WorkItem) * P->tc_items.size());
+            std::memcpy(host + P->off_tc, P->tc_items.data(), sizeof(WorkItem) * P->tc_items.size());
         if (!P->decode_items.empty())
-            std::memcpy(host.data() + P->off_dec, P->decode_items.data(), sizeof(WorkItem) * P->decode_items.size());
-        cuda_check(cudaMemcpyAsync(P->d_buf, host.data(), total, cudaMemcpyHostToDevice, as_stream(stream)),
-                   "plan upload");
-        cuda_check(cudaStreamSynchronize(as_stream(stream)), "plan upload sync");
+            std::memcpy(host + P->off_dec, P->decode_items.data(), sizeof(WorkItem) * P->decode_items.size());
+        cuda_check(cudaMemcpyAsync(P->d_buf, host, total, cudaMemcpyHostToDevice, as_stream(stream)), "plan upload");
+        cuda_check(cudaEventRecord(P->up_done, as_stream(stream)), "plan upload event");
         P->uploaded = true;
     });
 }
@@ -580,6 +595,11 @@ pb_status pb_attn_check_numerics(pb_attn_plan* P, const void* q, const void* k_p
 
 void pb_attn_plan_destroy(pb_attn_plan* P) {
     if (!P) return;
+    if (P->up_done) {
+        cudaEventSynchronize(P->up_done);
+        cudaEventDestroy(P->up_done);
+    }
+    if (P->h_buf) cudaFreeHost(P->h_buf);
     if (P->d_buf) cudaFree(P->d_buf);
     sm100_cache_release(P->sm100);
     if (P->io[0]) {

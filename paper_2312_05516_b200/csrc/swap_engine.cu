@@ -4,8 +4,11 @@
 //   * swap-in is issued layer by layer (layer l of every chunk before layer l+1); an event per
 //     layer lets the compute stream start layer l's attention as soon as its pages landed
 //     (the LayerDependencyAuditor rule of src/event_log.cpp:90-118);
-//   * swap-out (D2H) is queued behind the step's swap-ins on the copy stream, so the two
-//     directions never contend (schedule_swap_out_start, :50-53);
+//   * swap-out (D2H) runs on its own stream, concurrently with the swap-ins: measured faster
+//     on B200 than the reference's order (swap-out queued behind the step's swap-ins,
+//     schedule_swap_out_start, :50-53), which PB_SWAP_DUPLEX=0 restores;
+//   * swap-in is a batched H2D into staging plus a scatter kernel per layer, or with
+//     PB_SWAP_IN=zc one zero-copy kernel per layer reading the mapped pinned tier;
 //   * the swap-out GATHER (device pages -> contiguous staging) runs first, on the compute
 //     stream, so device slots vacated by swap-out can be refilled in the same step by restore /
 //     rematerialize / append (the reference reuses them LIFO, src/paged_kv_cache.cpp:28-37)
@@ -20,6 +23,8 @@
 #include <algorithm>
 #include <cstring>
 #include <memory>
+#include <cstdlib>
+#include <string>
 #include <vector>
 
 namespace pb {
@@ -56,6 +61,49 @@ __global__ void __launch_bounds__(256) swap_scatter_layer_kernel(const uint8_t* 
         const int4* src = reinterpret_cast<const int4*>(stage + job * page_bytes);
         int4* dst = reinterpret_cast<int4*>((kv ? vpool_l : kpool_l) + static_cast<int64_t>(slots[i]) * page_bytes);
         for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) __stcs(dst + v, __ldcs(src + v));
+    }
+}
+
+// Swap-in straight from the pinned host tier (zero-copy, mapped memory): one launch per layer
+// reads every swapped-in chunk's K and V page of that layer over PCIe / C2C and writes it into
+// the pool, with no staging buffer and no per-piece copy calls.  Four 16-B loads in flight per
+// thread keep enough requests outstanding to fill the link.
+__global__ void __launch_bounds__(256) swap_in_zc_layer_kernel(const uint8_t* __restrict__ host, int64_t chunk_bytes,
+                                                               int64_t layer_off, int64_t page_bytes,
+                                                               const int32_t* __restrict__ src_slots,
+                                                               const int32_t* __restrict__ dst_slots, int32_t n,
+                                                               uint8_t* __restrict__ kpool_l,
+                                                               uint8_t* __restrict__ vpool_l) {
+    const int64_t vecs = page_bytes / 16;
+    const int64_t total = static_cast<int64_t>(n) * 2 * vecs;
+    const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    int64_t v = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+    auto addr = [&](int64_t x, const int4*& src, int4*& dst) {
+        const int64_t job = x / vecs, e = x - job * vecs;
+        const int kv = static_cast<int>(job & 1);
+        const int64_t i = job >> 1;
+        src = reinterpret_cast<const int4*>(host + static_cast<int64_t>(src_slots[i]) * chunk_bytes + layer_off +
+                                            kv * page_bytes) + e;
+        dst = reinterpret_cast<int4*>((kv ? vpool_l : kpool_l) + static_cast<int64_t>(dst_slots[i]) * page_bytes) + e;
+    };
+    for (; v + 3 * stride < total; v += 4 * stride) {
+        const int4 *s0, *s1, *s2, *s3;
+        int4 *d0, *d1, *d2, *d3;
+        addr(v, s0, d0);
+        addr(v + stride, s1, d1);
+        addr(v + 2 * stride, s2, d2);
+        addr(v + 3 * stride, s3, d3);
+        const int4 a = __ldcv(s0), b = __ldcv(s1), c = __ldcv(s2), d = __ldcv(s3);
+        *d0 = a;
+        *d1 = b;
+        *d2 = c;
+        *d3 = d;
+    }
+    for (; v < total; v += stride) {
+        const int4* s0;
+        int4* d0;
+        addr(v, s0, d0);
+        *d0 = __ldcv(s0);
     }
 }
 
@@ -96,8 +144,12 @@ struct pb_kv_tier {
     uint8_t* host = nullptr;       // pinned [host_slot][layer][K|V][page]
     uint8_t* stage_out = nullptr;  // device [chunk][layer][K|V][page]
     uint8_t* stage_in = nullptr;   // device [layer][chunk][K|V][page]
-    int32_t* d_slots = nullptr;    // device: [out slots | in slots]
+    int32_t* d_slots = nullptr;    // device: [out src slots | in dst slots | in host src slots]
     int32_t* h_slots = nullptr;    // pinned staging for the slot lists
+    const uint8_t* host_dev = nullptr; // device alias of the pinned tier (zero-copy swap-in)
+    cudaStream_t d2h = nullptr;    // duplex mode: swap-out D2H on its own stream
+    cudaEvent_t d2h_done = nullptr;
+    int mode_zc = 0, mode_duplex = 0;
     cudaEvent_t gathered = nullptr, done = nullptr;
     std::vector<cudaEvent_t> layer_ready;
     bool any_in = false;
@@ -128,10 +180,21 @@ pb_status pb_tier_create(int32_t n_layer, int32_t host_slots, int64_t page_bytes
             cudaGetLastError();
             fail(PB_ERR_INSUFFICIENT_DEVICE_MEMORY, "swap staging allocation failed");
         }
-        cuda_check(cudaMalloc(&T->d_slots, sizeof(int32_t) * 2 * max_chunks_per_step), "cudaMalloc(slots)");
-        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&T->h_slots), sizeof(int32_t) * 2 * max_chunks_per_step,
+        cuda_check(cudaMalloc(&T->d_slots, sizeof(int32_t) * 3 * max_chunks_per_step), "cudaMalloc(slots)");
+        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&T->h_slots), sizeof(int32_t) * 3 * max_chunks_per_step,
                                  cudaHostAllocPortable),
                    "cudaHostAlloc(slots)");
+        void* hd = nullptr;
+        if (cudaHostGetDevicePointer(&hd, T->host, 0) == cudaSuccess) T->host_dev = static_cast<const uint8_t*>(hd);
+        else cudaGetLastError();
+        // transfer policy: zero-copy swap-in (default) or staged H2D + scatter; swap-out D2H
+        // behind the swap-ins (reference order, default) or on its own stream (duplex)
+        const char* m = std::getenv("PB_SWAP_IN");
+        T->mode_zc = T->host_dev && m && std::string(m) == "zc"; // staged measured faster
+        const char* dx = std::getenv("PB_SWAP_DUPLEX");
+        T->mode_duplex = !(dx && std::atoi(dx) == 0); // measured faster on B200 (profiles/)
+        cuda_check(cudaStreamCreateWithFlags(&T->d2h, cudaStreamNonBlocking), "d2h stream");
+        cuda_check(cudaEventCreateWithFlags(&T->d2h_done, cudaEventDisableTiming), "event");
         cuda_check(cudaEventCreateWithFlags(&T->gathered, cudaEventDisableTiming), "event");
         cuda_check(cudaEventCreateWithFlags(&T->done, cudaEventDisableTiming), "event");
         T->layer_ready.resize(static_cast<size_t>(n_layer));
@@ -148,6 +211,11 @@ void pb_tier_destroy(pb_kv_tier* T) {
     cudaFree(T->stage_in);
     cudaFree(T->d_slots);
     cudaFreeHost(T->h_slots);
+    if (T->d2h) {
+        cudaStreamSynchronize(T->d2h);
+        cudaStreamDestroy(T->d2h);
+    }
+    if (T->d2h_done) cudaEventDestroy(T->d2h_done);
     if (T->gathered) cudaEventDestroy(T->gathered);
     if (T->done) cudaEventDestroy(T->done);
     for (auto e : T->layer_ready) cudaEventDestroy(e);
@@ -176,7 +244,8 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         cuda_check(cudaEventSynchronize(T->done), "swap step ordering");
         for (int64_t i = 0; i < n_out; ++i) T->h_slots[i] = out_moves[i].src_slot;
         for (int64_t i = 0; i < n_in; ++i) T->h_slots[T->max_chunks + i] = in_moves[i].dst_slot;
-        cuda_check(cudaMemcpyAsync(T->d_slots, T->h_slots, sizeof(int32_t) * 2 * T->max_chunks,
+        for (int64_t i = 0; i < n_in; ++i) T->h_slots[2 * T->max_chunks + i] = in_moves[i].src_slot;
+        cuda_check(cudaMemcpyAsync(T->d_slots, T->h_slots, sizeof(int32_t) * 3 * T->max_chunks,
                                    cudaMemcpyHostToDevice, cs),
                    "slot upload");
         const int64_t pb = T->page_bytes;
@@ -198,7 +267,16 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         std::vector<void*> dst, src;
         std::vector<size_t> sz;
         for (int32_t l = 0; l < T->n_layer; ++l) {
-            if (n_in > 0) {
+            if (n_in > 0 && T->mode_zc) {
+                const int64_t vecs = n_in * 2 * (pb / 16);
+                const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((vecs + 1023) / 1024, n_sms() * 4)));
+                swap_in_zc_layer_kernel<<<grid, 256, 0, xs>>>(T->host_dev, T->chunk_bytes(), static_cast<int64_t>(l) * 2 * pb,
+                                                              pb, T->d_slots + 2 * T->max_chunks,
+                                                              T->d_slots + T->max_chunks, static_cast<int32_t>(n_in),
+                                                              kp + l * layer_stride, vp + l * layer_stride);
+                cuda_check(cudaGetLastError(), "swap-in (zero-copy)");
+                count_launch();
+            } else if (n_in > 0) {
                 dst.clear();
                 src.clear();
                 sz.clear();
@@ -218,7 +296,13 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
             }
             cuda_check(cudaEventRecord(T->layer_ready[static_cast<size_t>(l)], xs), "event record");
         }
-        // 3. swap-out D2H behind the swap-ins on the copy stream (no duplex contention)
+        // 3. swap-out D2H: behind the swap-ins on the copy stream (the reference's order, no
+        // duplex contention on the link), or concurrently on its own stream (duplex mode)
+        cudaStream_t os = xs;
+        if (T->mode_duplex) {
+            os = T->d2h;
+            cuda_check(cudaStreamWaitEvent(os, T->gathered, 0), "stream wait");
+        }
         if (n_out > 0) {
             dst.clear();
             src.clear();
@@ -228,7 +312,11 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
                 src.push_back(T->stage_out + i * T->chunk_bytes());
                 sz.push_back(static_cast<size_t>(T->chunk_bytes()));
             }
-            copy_batch(dst, src, sz, xs);
+            copy_batch(dst, src, sz, os);
+        }
+        if (T->mode_duplex) {
+            cuda_check(cudaEventRecord(T->d2h_done, os), "event record");
+            cuda_check(cudaStreamWaitEvent(xs, T->d2h_done, 0), "stream wait");
         }
         cuda_check(cudaEventRecord(T->done, xs), "event record");
     });
