@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         e = a;
                     } else if (PB_POLY_EVERY > 0 && ((c >> 1) % (PB_POLY_EVERY > 0 ? PB_POLY_EVERY : 1)) ==
                                                         PB_POLY_EVERY - 1) {
-                        e = exp2_poly3_x2(a);
+                        e = exp2_neg_poly_x2(a);
                     } else {
                         e.x = ex2(a.x);
                         e.y = ex2(a.y);

@@ -243,6 +243,22 @@ __device__ __forceinline__ float2 exp2_poly3_x2(float2 x) {
     return y;
 }
 
+// Cheaper 2^x on a pair for x <= 0: clamp at -127, round with the 1.5*2^23 magic add, cubic
+// with p(0) = 1 exactly (max rel. err 1.02e-4 on [-0.5, 0.5], far below bf16's 3.9e-3), and
+// the integer part added into the exponent (so x = -127, incl. masked -inf, gives exactly 0).
+// ~10 issue slots per pair, all on the FMA / ALU pipes.
+__device__ __forceinline__ float2 exp2_neg_poly_x2(float2 x) {
+    const float2 xc = make_float2(fmaxf(x.x, -127.f), fmaxf(x.y, -127.f));
+    const float2 r = add2(xc, make_float2(12582912.f, 12582912.f));
+    const float2 t = add2(r, make_float2(-12582912.f, -12582912.f));
+    const float2 f = fma2(t, make_float2(-1.f, -1.f), xc);
+    float2 p = fma2(make_float2(0.055007655f, 0.055007655f), f, make_float2(0.24220793f, 0.24220793f));
+    p = fma2(p, f, make_float2(0.69328272f, 0.69328272f));
+    p = fma2(p, f, make_float2(1.f, 1.f));
+    return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23)),
+                       __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23)));
+}
+
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
     uint32_t r;
     asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
