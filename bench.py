@@ -466,6 +466,34 @@ def bench_config5(args):
     clk = clocks.stop()
     total_ms = t0.elapsed_time(t1)
     swap_ms = sum(a.elapsed_time(b) for a, b in swap_ev)
+
+    # the two halves alone, same steps: attention without swaps, swaps without attention
+    def timed_loop(fn):
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(cs)
+        for s in range(args.steps):
+            fn(args.warmup + s)
+        xs.wait_stream(cs)
+        cs.wait_stream(xs)
+        b.record(cs)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / args.steps
+
+    def attn_only(i):
+        pl = plans[i]
+        pl.upload(cs.cuda_stream)
+        for l in range(n_layer):
+            pl.run(q.data_ptr(), k.data_ptr() + l * layer_stride, v.data_ptr() + l * layer_stride, out.data_ptr(),
+                   wsb.data_ptr(), cs.cuda_stream)
+
+    def swap_only(i):
+        p = steps[i]
+        tier.step(k.data_ptr(), v.data_ptr(), layer_stride, p.out_moves, p.in_moves, cs.cuda_stream, xs.cuda_stream)
+        tier.wait_layer(n_layer - 1, cs.cuda_stream)
+
+    attn_only_ms = timed_loop(attn_only)
+    swap_only_ms = timed_loop(swap_only)
     timed = steps[args.warmup:args.warmup + args.steps]
     attn_bytes = sum(pl.stats()["bytes"] for pl in plans[args.warmup:args.warmup + args.steps]) * n_layer
     attn_flops = sum(pl.stats()["flops"] for pl in plans[args.warmup:args.warmup + args.steps]) * n_layer
@@ -497,6 +525,8 @@ def bench_config5(args):
         "roofline": {"bound": "hbm", "achieved": value, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": value / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_src,
                      "tflops": attn_flops / (total_ms / 1e3) / 1e12},
+        "parts_ms_per_step": {"attention_only": attn_only_ms, "swap_only": swap_only_ms,
+                              "both": total_ms / args.steps},
         "swap": {"chunks_in": n_in, "chunks_out": n_out, "bytes": swap_bytes,
                  "copy_stream_gbs": swap_bytes / (swap_ms / 1e3) / 1e9 if swap_ms > 0 else None,
                  "pinned_h2d_peak_gbs": h2d_peak, "pinned_d2h_peak_gbs": d2h_peak},

@@ -432,9 +432,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const bool diag = kv0 + kBN > allowed;
                 float pm[8];
 #pragma unroll
-                for (int c = 0; c < kBN / 32; ++c)
-                    tmem_ld32(t_lane + col_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
-                tmem_ld_wait();
+                if (p.ablate == 4) { // profiling: half the S read (columns 32..63 reuse 0..31)
+                    tmem_ld32(t_lane + col_s, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
+                    tmem_ld_wait();
+#pragma unroll
+                    for (int c = 32; c < kBN; ++c) x[c] = x[c - 32] * 0.5f;
+                } else {
+#pragma unroll
+                    for (int c = 0; c < kBN / 32; ++c)
+                        tmem_ld32(t_lane + col_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
+                    tmem_ld_wait();
+                }
                 // causal mask (only tiles that cross this row's boundary) + running max
                 if (diag) {
 #pragma unroll
@@ -484,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pk[c >> 1] = pack_bf16x2(e.x, e.y);
                 }
                 // P (bf16) over the first kBN/2 columns of this S buffer
-                tmem_st32(t_lane + col_s, pk);
+                if (p.ablate != 5) tmem_st32(t_lane + col_s, pk); // 5: profiling, P not stored
                 // PV_t of the previous tile must be complete before O_t is rescaled and before
                 // P_t(j) is released; waiting on it every tile also keeps pv_done at most one
                 // phase behind, so its parity wait is exact

@@ -30,6 +30,8 @@
 namespace pb {
 namespace {
 
+constexpr int kDefaultLayerBlock = 8; // swap-in H2D pieces of 8 layers (measured best of 1, 2, 4, 8, 40)
+
 __global__ void __launch_bounds__(256) swap_gather_kernel(const uint8_t* __restrict__ kpool,
                                                           const uint8_t* __restrict__ vpool, int64_t layer_stride,
                                                           int64_t page_bytes, const int32_t* __restrict__ slots,
@@ -44,22 +46,6 @@ __global__ void __launch_bounds__(256) swap_gather_kernel(const uint8_t* __restr
         const int4* src = reinterpret_cast<const int4*>((kv ? vpool : kpool) + l * layer_stride +
                                                         static_cast<int64_t>(slots[i]) * page_bytes);
         int4* dst = reinterpret_cast<int4*>(stage + job * page_bytes);
-        for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) __stcs(dst + v, __ldcs(src + v));
-    }
-}
-
-__global__ void __launch_bounds__(256) swap_scatter_layer_kernel(const uint8_t* __restrict__ stage,
-                                                                 uint8_t* __restrict__ kpool_l,
-                                                                 uint8_t* __restrict__ vpool_l, int64_t page_bytes,
-                                                                 const int32_t* __restrict__ slots, int32_t n) {
-    // staging for one layer: [chunk i][K|V][page]
-    const int64_t jobs = static_cast<int64_t>(n) * 2;
-    const int64_t vecs = page_bytes / 16;
-    for (int64_t job = blockIdx.x; job < jobs; job += gridDim.x) {
-        const int kv = static_cast<int>(job & 1);
-        const int64_t i = job >> 1;
-        const int4* src = reinterpret_cast<const int4*>(stage + job * page_bytes);
-        int4* dst = reinterpret_cast<int4*>((kv ? vpool_l : kpool_l) + static_cast<int64_t>(slots[i]) * page_bytes);
         for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) __stcs(dst + v, __ldcs(src + v));
     }
 }
@@ -107,6 +93,26 @@ __global__ void __launch_bounds__(256) swap_in_zc_layer_kernel(const uint8_t* __
     }
 }
 
+// Scatter of one block of nl layers: staging [chunk i][layer ll][K|V][page] -> the pools of
+// layers layer0 .. layer0+nl-1.
+__global__ void __launch_bounds__(256) swap_scatter_block_kernel(const uint8_t* __restrict__ stage,
+                                                                 uint8_t* __restrict__ kpool, uint8_t* __restrict__ vpool,
+                                                                 int64_t layer_stride, int32_t layer0, int32_t nl,
+                                                                 int64_t page_bytes, const int32_t* __restrict__ slots,
+                                                                 int32_t n) {
+    const int64_t jobs = static_cast<int64_t>(n) * nl * 2;
+    const int64_t vecs = page_bytes / 16;
+    for (int64_t job = blockIdx.x; job < jobs; job += gridDim.x) {
+        const int kv = static_cast<int>(job & 1);
+        const int64_t il = job >> 1;
+        const int64_t i = il / nl, ll = il % nl;
+        const int4* src = reinterpret_cast<const int4*>(stage + job * page_bytes);
+        int4* dst = reinterpret_cast<int4*>((kv ? vpool : kpool) + (layer0 + ll) * layer_stride +
+                                            static_cast<int64_t>(slots[i]) * page_bytes);
+        for (int64_t v = threadIdx.x; v < vecs; v += blockDim.x) __stcs(dst + v, __ldcs(src + v));
+    }
+}
+
 int n_sms() {
     static int s = 0;
     if (!s) {
@@ -150,6 +156,7 @@ struct pb_kv_tier {
     cudaStream_t d2h = nullptr;    // duplex mode: swap-out D2H on its own stream
     cudaEvent_t d2h_done = nullptr;
     int mode_zc = 0, mode_duplex = 0;
+    int layer_block = 1;           // staged swap-in: layers per H2D piece (larger pieces, coarser events)
     cudaEvent_t gathered = nullptr, done = nullptr;
     std::vector<cudaEvent_t> layer_ready;
     bool any_in = false;
@@ -193,6 +200,8 @@ pb_status pb_tier_create(int32_t n_layer, int32_t host_slots, int64_t page_bytes
         T->mode_zc = T->host_dev && m && std::string(m) == "zc"; // staged measured faster
         const char* dx = std::getenv("PB_SWAP_DUPLEX");
         T->mode_duplex = !(dx && std::atoi(dx) == 0); // measured faster on B200 (profiles/)
+        const char* lb = std::getenv("PB_SWAP_LB");
+        T->layer_block = std::max(1, std::min(n_layer, lb ? std::atoi(lb) : kDefaultLayerBlock));
         cuda_check(cudaStreamCreateWithFlags(&T->d2h, cudaStreamNonBlocking), "d2h stream");
         cuda_check(cudaEventCreateWithFlags(&T->d2h_done, cudaEventDisableTiming), "event");
         cuda_check(cudaEventCreateWithFlags(&T->gathered, cudaEventDisableTiming), "event");
@@ -276,20 +285,23 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
                                                               kp + l * layer_stride, vp + l * layer_stride);
                 cuda_check(cudaGetLastError(), "swap-in (zero-copy)");
                 count_launch();
-            } else if (n_in > 0) {
+            } else if (n_in > 0 && l % T->layer_block == 0) {
+                // one H2D piece per chunk for the next nl layers (contiguous in the host tier),
+                // then one scatter for the block; every layer of the block is ready after it
+                const int32_t nl = std::min(T->layer_block, T->n_layer - l);
                 dst.clear();
                 src.clear();
                 sz.clear();
-                uint8_t* stage_l = T->stage_in + static_cast<int64_t>(l) * n_in * 2 * pb;
+                uint8_t* stage_b = T->stage_in + static_cast<int64_t>(l) * n_in * 2 * pb;
                 for (int64_t i = 0; i < n_in; ++i) {
-                    dst.push_back(stage_l + i * 2 * pb);
+                    dst.push_back(stage_b + i * nl * 2 * pb);
                     src.push_back(T->host + static_cast<int64_t>(in_moves[i].src_slot) * T->chunk_bytes() +
                                   static_cast<int64_t>(l) * 2 * pb);
-                    sz.push_back(static_cast<size_t>(2 * pb));
+                    sz.push_back(static_cast<size_t>(nl * 2 * pb));
                 }
                 copy_batch(dst, src, sz, xs);
-                const int grid = static_cast<int>(std::min<int64_t>(n_in * 2, n_sms() * 4));
-                swap_scatter_layer_kernel<<<grid, 256, 0, xs>>>(stage_l, kp + l * layer_stride, vp + l * layer_stride, pb,
+                const int grid = static_cast<int>(std::min<int64_t>(n_in * nl * 2, n_sms() * 4));
+                swap_scatter_block_kernel<<<grid, 256, 0, xs>>>(stage_b, kp, vp, layer_stride, l, nl, pb,
                                                                T->d_slots + T->max_chunks, static_cast<int32_t>(n_in));
                 cuda_check(cudaGetLastError(), "swap scatter");
                 count_launch();
