@@ -12,6 +12,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <memory>
 #include <mutex>
 #include <string>
@@ -231,8 +232,30 @@ void build_work(pb_attn_plan& P) {
     auto lpt = [](auto& v) {
         std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
     };
-    lpt(tc_list);
     lpt(dec_list);
+    static const int tile_order = [] { // 1 (default): items of one (span, kv head) together
+        const char* e = std::getenv("PB_TILE_ORDER");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (tile_order == 1 && !tc_list.empty()) {
+        // The query blocks of one (span, kv head) stream the same K/V pages: keeping them
+        // adjacent in the queue lets concurrently running CTAs share those pages through L2.
+        // Groups go heaviest first (by their heaviest item), items heaviest first inside.
+        std::map<std::pair<int32_t, int32_t>, double> gmax;
+        for (auto& e : tc_list) {
+            auto& m = gmax[{e.second.span, e.second.kvh}];
+            m = std::max(m, e.first);
+        }
+        std::stable_sort(tc_list.begin(), tc_list.end(), [&](const auto& a, const auto& b) {
+            const double ga = gmax[{a.second.span, a.second.kvh}], gb = gmax[{b.second.span, b.second.kvh}];
+            if (ga != gb) return ga > gb;
+            if (a.second.span != b.second.span) return a.second.span < b.second.span;
+            if (a.second.kvh != b.second.kvh) return a.second.kvh < b.second.kvh;
+            return a.first > b.first;
+        });
+    } else {
+        lpt(tc_list);
+    }
     if (P.fused) {
         // share of the launch's SM time the decode queue needs (est. cycles); the fused kernel
         // starts that share of its CTAs on decode units, the rest steal once their queue is dry

@@ -364,3 +364,18 @@ def test_fused_append_equals_append_then_attention(gh, cuda, case):
     assert torch.equal(k1, k2) and torch.equal(v1, v2)
     n = w.total_tokens * w.n_head * w.head_size
     assert np.array_equal(out.float().cpu().numpy()[:n], want)
+
+
+@pytest.mark.parametrize("chunk", [8, 32, 64, 128])
+def test_bf16_page_sizes(gh, oracle, chunk):
+    """Page sizes other than 16 (the reference's chunk_size is a parameter): 8..64 run on the
+    tcgen05 tile and decode paths, 128 on the SIMT path; all within the bf16 tolerance."""
+    rng = SplitMix64(500 + chunk)
+    for trial in range(2):
+        w = random_instance(rng, 16, 4, 128, chunk, PB_BF16, 10, 1300, all_decode=(trial == 1), max_q=150)
+        q, k, v = gh.device_inputs(w)
+        got, plan = gh.run_plan(w, q, k, v)
+        st, want = oracle.attention(w.shape(), w.batch(), w.host_q(), w.host_pool("k"), w.host_pool("v"))
+        assert st == 0
+        ok, err = gh.bf16_close(got, want)
+        assert ok, (chunk, trial, err, plan.stats())
