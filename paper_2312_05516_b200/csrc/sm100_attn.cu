@@ -42,10 +42,17 @@ namespace {
 
 using namespace pb::sm100;
 
-constexpr int kThreads = 384; // WG0/WG1 softmax of tiles A/B, WG2: TMA warp, MMA warp, 2 spare
+#ifndef PB_SPLIT
+#define PB_SPLIT 0 // 1: two softmax warpgroups per query tile (each takes half of the S columns)
+#endif
+constexpr int kHalves = PB_SPLIT ? 2 : 1;
+constexpr int kSoftWG = 2 * kHalves;          // softmax warpgroups (query tiles A/B x halves)
+constexpr int kThreads = 128 * (kSoftWG + 1); // + one warpgroup: TMA warp, MMA warp, 2 spare
+constexpr int kProdWarp = 4 * kSoftWG;
+constexpr int kMmaWarp = kProdWarp + 1;
 constexpr int kTileRows = 128;        // M rows per query tile
 constexpr int kBN = 64;               // kv rows per kv tile (N of S = Q K^T, K of O += P V)
-constexpr int kKvStages = 3;          // K ring and V ring depth (kBN-row tiles)
+constexpr int kKvStages = 4;          // K ring and V ring depth (kBN-row tiles)
 constexpr uint32_t kTmemCols = 512;   // S_A[2] [0,128) S_B[2] [128,256) O_A [256,384) O_B [384,512)
 constexpr uint32_t kColO = 256;
 #ifndef PB_SETMAXNREG
@@ -53,11 +60,17 @@ constexpr uint32_t kColO = 256;
 #endif
 constexpr bool kUseSetMaxNReg = PB_SETMAXNREG != 0;
 #ifndef PB_REG_LO
-#define PB_REG_LO 88  // WG2 after setmaxnreg.dec
+#define PB_REG_LO (PB_SPLIT ? 56 : 88) // producer/MMA warpgroup after setmaxnreg.dec
 #endif
 #ifndef PB_REG_HI
-#define PB_REG_HI 208 // softmax groups after setmaxnreg.inc (128*LO + 256*HI <= 64K)
+#define PB_REG_HI (PB_SPLIT ? 104 : 208) // softmax warpgroups after setmaxnreg.inc
 #endif
+// setmaxnreg only moves registers inside the CTA's launch allocation (kThreads x the
+// per-thread count __launch_bounds__ gives, 64K / kThreads rounded down to 8): what the
+// softmax warpgroups gain must be what the producer/MMA warpgroup gives up, or inc blocks
+constexpr int kLaunchRegs = (65536 / (128 * ((PB_SPLIT ? 4 : 2) + 1))) / 8 * 8;
+static_assert((PB_REG_HI - kLaunchRegs) * (PB_SPLIT ? 4 : 2) <= (kLaunchRegs - PB_REG_LO),
+              "setmaxnreg budget exceeds the launch register allocation");
 constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max grows by > 2^8
 #ifndef PB_POLY_EVERY
 #define PB_POLY_EVERY 0 // one exp2 pair in N on the FMA pipe; 0 = all on MUFU (measured fastest, see profiles/)
@@ -68,17 +81,24 @@ constexpr int kMaxPpt = kBN / 8; // pages per kv tile (page_tokens >= 8)
 
 template <int D>
 struct __align__(1024) Smem {
-    uint8_t q[2][2][kTileRows * D * 2];   // [item parity][tile A, B]: [D/64][128 rows][128 B] K-major SW128
+    uint8_t q[2][kTileRows * D * 2];      // tiles A, B: [D/64][128 rows][128 B] K-major SW128
     uint8_t k[kKvStages][kBN * D * 2];    // ring of kv tiles: [D/64][64 rows][128 B] K-major SW128
     uint8_t v[kKvStages][kBN * D * 2];    // same layout, read as the MN-major SW128 B operand
-    uint64_t q_full[2], q_empty[2];       // per item parity (the next item's Q loads early)
+    uint64_t q_full, q_empty;             // Q is released after the item's last S MMA
     uint64_t k_full[kKvStages], k_empty[kKvStages], v_full[kKvStages], v_empty[kKvStages];
     uint64_t s_full[2][2];                // [query tile][S buffer]
     uint64_t p_full[2], pv_done[2], o_ready[2], o_empty[2]; // per query tile
     uint64_t item_full[kItemRing], item_empty[kItemRing];   // dynamic tile scheduler ring
     uint64_t drain;                       // MMA issuer: every commit of the pass has landed
     int32_t item_ring[kItemRing];
+    float red_m[2][2][kHalves][128];      // [S buffer][query tile][half][row] partial row max
+    float red_l[2][kHalves][128];         // [query tile][half][row] partial row sum
 };
+
+// one CTA per SM: the larger of the two layouts plus 1 KiB of alignment slack must fit the
+// 227 KiB opt-in shared memory of an sm_100 CTA
+static_assert(sizeof(Smem<128>) + 1024 <= 232448, "tile layout exceeds shared memory");
+static_assert(sizeof(dtc::DtSmem) + 1024 <= 232448, "decode layout exceeds shared memory");
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
 
@@ -112,10 +132,8 @@ __device__ __forceinline__ void umma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, u
 
 template <int D>
 __device__ __forceinline__ void tile_init(Smem<D>& s) { // thread 0
-    mbar_init(&s.q_full[0], 1);
-    mbar_init(&s.q_full[1], 1);
-    mbar_init(&s.q_empty[0], 1);
-    mbar_init(&s.q_empty[1], 1);
+    mbar_init(&s.q_full, 1);
+    mbar_init(&s.q_empty, 1);
     for (int i = 0; i < kKvStages; ++i) {
         mbar_init(&s.k_full[i], 1);
         mbar_init(&s.k_empty[i], 1);
@@ -125,20 +143,20 @@ __device__ __forceinline__ void tile_init(Smem<D>& s) { // thread 0
     for (int i = 0; i < 2; ++i) {
         mbar_init(&s.s_full[i][0], 1);
         mbar_init(&s.s_full[i][1], 1);
-        mbar_init(&s.p_full[i], 128);
+        mbar_init(&s.p_full[i], 128 * kHalves);
         mbar_init(&s.pv_done[i], 1);
         mbar_init(&s.o_ready[i], 1);
-        mbar_init(&s.o_empty[i], 128);
+        mbar_init(&s.o_empty[i], 128 * kHalves);
     }
     for (int i = 0; i < kItemRing; ++i) {
         mbar_init(&s.item_full[i], 1);
-        mbar_init(&s.item_empty[i], 1 + 8); // MMA thread + the 8 softmax warps
+        mbar_init(&s.item_empty[i], 1 + 4 * kSoftWG); // MMA thread + the softmax warps
     }
     mbar_init(&s.drain, 1);
 }
 template <int D>
 __device__ __forceinline__ void tile_inval(Smem<D>& s) { // thread 0, pipeline drained
-    uint64_t* first = &s.q_full[0];
+    uint64_t* first = &s.q_full;
     uint64_t* last = &s.drain;
     for (uint64_t* b = first; b <= last; ++b) mbar_inval(b);
 }
@@ -178,7 +196,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch(&tm_v);
         tma_prefetch(&tm_qd);
     }
-    if (warp == 9) tmem_alloc<kTmemCols>(&tmem_base_sh);
+    if (warp == kMmaWarp) tmem_alloc<kTmemCols>(&tmem_base_sh);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
@@ -215,7 +233,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 p.trace[(static_cast<size_t>(blockIdx.x) * 2 + (dec == dec_first ? 0 : 1)) * 4 + 3] = gtime();
         }
     };
-    if (wg == 2) {
+    if (wg == kSoftWG) {
     if (kUseSetMaxNReg) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(PB_REG_LO) : "memory");
     for (int pass = 0; pass < 2; ++pass) {
     const bool dec = (pass == 0) == dec_first;
@@ -223,8 +241,9 @@ __global__ void __launch_bounds__(kThreads, 1)
     mode_begin(dec);
     if (dec) {
         if constexpr (D == 128)
-            dtc::decode_cta_run<GD>(ds, tmem, &tm_qd, &tm_k, &tm_v, p, p.dec_items, p.n_dec_items, ctr + 4, 8, 9, 0);
-    } else if (warp == 8) {
+            dtc::decode_cta_run<GD>(ds, tmem, &tm_qd, &tm_k, &tm_v, p, p.dec_items, p.n_dec_items, ctr + 4, kProdWarp,
+                                    kMmaWarp, 0);
+    } else if (warp == kProdWarp) {
         // ============================ TMA producer ============================
         if (elect_one()) {
             int it = 0, kst = 0, vst = 0;
@@ -245,14 +264,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (item < 0) break;
                 const WorkItem w = p.items[item];
                 const SpanDev sp = p.spans[w.span];
-                const int qs = it & 1; // Q buffer set of this item
-                if (it >= 2) mbar_wait(&s.q_empty[qs], ((it >> 1) - 1) & 1);
+                if (it > 0) mbar_wait(&s.q_empty, (it - 1) & 1);
                 const ItemTiles T = item_tiles(w, sp, tpt);
-                mbar_arrive_expect_tx(&s.q_full[qs], q_bytes * (T.nt[1] > 0 ? 2u : 1u));
+                mbar_arrive_expect_tx(&s.q_full, q_bytes * (T.nt[1] > 0 ? 2u : 1u));
                 for (int t = 0; t < 2; ++t)
                     if (T.nt[t] > 0)
                         for (int h = 0; h < KH; ++h)
-                            tma_load_3d(s.q[qs][t] + h * kHalfBytes, &tm_q, &s.q_full[qs], h * 64, w.kvh * g,
+                            tma_load_3d(s.q[t] + h * kHalfBytes, &tm_q, &s.q_full, h * 64, w.kvh * g,
                                         sp.query_start + w.t0 + t * tpt);
                 const int32_t* table = p.block_tables + sp.bt_off;
                 const int n_pages = sp.n_pages;
@@ -287,7 +305,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
-    } else if (warp == 9) {
+    } else if (warp == kMmaWarp) {
         // ============================ MMA issuer =============================
         if (elect_one()) {
             constexpr uint32_t idesc_s = umma_idesc_bf16(128, kBN, false, false);
@@ -310,8 +328,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const WorkItem w = p.items[item];
                 const SpanDev sp = p.spans[w.span];
                 const ItemTiles T = item_tiles(w, sp, tpt);
-                const int qs = it & 1;
-                mbar_wait(&s.q_full[qs], (it >> 1) & 1);
+                mbar_wait(&s.q_full, it & 1);
                 tc_fence_after();
                 // S_t(jj) = Q_t K(jj)^T into group t's S buffer (c_s[t] & 1), for every group that
                 // needs kv tile jj.  Descriptors are advanced by adding (byte offset >> 4) to the
@@ -322,7 +339,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     const uint64_t kd = umma_desc_sw128(smem_u32(s.k[kst]), 16, 1024);
                     for (int t = 0; t < 2; ++t) {
                         if (jj >= T.ntiles[t]) continue;
-                        const uint64_t qd = umma_desc_sw128(smem_u32(s.q[qs][t]), 16, 1024);
+                        const uint64_t qd = umma_desc_sw128(smem_u32(s.q[t]), 16, 1024);
                         const uint32_t b = c_s[t] & 1;
 #pragma unroll
                         for (int kk = 0; kk < D / 16; ++kk) {
@@ -335,7 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     }
                     umma_commit(&s.k_empty[kst]);
                     if (++kst == kKvStages) { kst = 0; kph ^= 1; }
-                    if (jj + 1 == T.n_kv) umma_commit(&s.q_empty[qs]); // Q read by S MMAs only
+                    if (jj + 1 == T.n_kv) umma_commit(&s.q_empty); // Q is read by S MMAs only
                 };
                 // S runs one kv tile ahead of PV: S(j+1) is computed while the softmax groups
                 // turn S(j) into P(j) (two S buffers per group)
@@ -378,19 +395,29 @@ __global__ void __launch_bounds__(kThreads, 1)
     mode_begin(dec);
     if (dec) {
         if constexpr (D == 128)
-            dtc::decode_cta_run<GD>(ds, tmem, &tm_qd, &tm_k, &tm_v, p, p.dec_items, p.n_dec_items, ctr + 4, 8, 9, 0);
+            dtc::decode_cta_run<GD>(ds, tmem, &tm_qd, &tm_k, &tm_v, p, p.dec_items, p.n_dec_items, ctr + 4, kProdWarp,
+                                    kMmaWarp, 0);
     } else {
         // ============ softmax / correction / epilogue (one group per query tile) ============
-        const int t = wg;                           // query tile of this warpgroup
+        // kHalves softmax warpgroups per query tile: warpgroup wg serves tile wg & 1 and the
+        // column half wg >> 1 of every S tile (same TMEM lanes, different columns); the two
+        // halves of a row agree on the running max through shared memory once per tile.
+        const int t = wg & 1;                       // query tile of this warpgroup
+        const int hf = wg >> 1;                     // column half (0 when kHalves == 1)
         const int quad = warp & 3;                  // TMEM lane quadrant of this warp
         const int row = quad * 32 + (threadIdx.x & 31);
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(quad * 32) << 16);
         const uint32_t col_o = kColO + t * 128;
+        constexpr int kCols = kBN / kHalves;        // S columns per thread per kv tile
+        constexpr int kOCols = D / kHalves;         // O columns per thread (rescale, epilogue)
         const float sl2 = p.scale_log2;
         uint32_t n_o = 0;
         uint32_t c_t = 0;     // kv tiles processed by this group (S buffer / barrier phase)
         uint32_t kv_seen = 0; // kv tiles loaded for earlier items (V ring position)
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
+        auto pair_sync = [&]() { // the two warps (one per half) that own these 32 rows
+            if constexpr (kHalves > 1) asm volatile("bar.sync %0, 64;" ::"r"(1 + t * 4 + quad) : "memory");
+        };
         for (int it = 0;; ++it) {
             const int slot = it % kItemRing;
             mbar_wait(&s.item_full[slot], (it / kItemRing) & 1);
@@ -409,7 +436,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             // never-written pool memory): this group zeroes them in the V stage of the item's
             // last kv tile before its PV reads it (tile A when it reaches that tile, else B),
             // so 0 * NaN cannot reach O
-            const bool zero_owner = (t == 0) ? (T.ntiles[0] == T.n_kv) : (T.ntiles[0] < T.n_kv);
+            const bool zero_owner = hf == 0 && ((t == 0) ? (T.ntiles[0] == T.n_kv) : (T.ntiles[0] < T.n_kv));
             const int t_local = row / g;
             const bool valid = t_local < T.nt[t] && row < g * tpt;
             const int tok0 = w.t0 + t * tpt;           // first span-relative token of this tile
@@ -427,38 +454,35 @@ __global__ void __launch_bounds__(kThreads, 1)
                     l_run = 1.f;
                     continue;
                 }
-                float x[kBN];
-                const int kv0 = j * kBN;
-                const bool diag = kv0 + kBN > allowed;
+                float x[kCols];
+                const int kv0 = j * kBN + hf * kCols;
+                const bool diag = kv0 + kCols > allowed;
                 float pm[8];
 #pragma unroll
-                if (p.ablate == 4) { // profiling: half the S read (columns 32..63 reuse 0..31)
-                    tmem_ld32(t_lane + col_s, *reinterpret_cast<uint32_t(*)[32]>(&x[0]));
-                    tmem_ld_wait();
-#pragma unroll
-                    for (int c = 32; c < kBN; ++c) x[c] = x[c - 32] * 0.5f;
-                } else {
-#pragma unroll
-                    for (int c = 0; c < kBN / 32; ++c)
-                        tmem_ld32(t_lane + col_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
-                    tmem_ld_wait();
-                }
+                for (int c = 0; c < kCols / 32; ++c)
+                    tmem_ld32(t_lane + col_s + hf * kCols + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
+                tmem_ld_wait();
                 // causal mask (only tiles that cross this row's boundary) + running max
                 if (diag) {
 #pragma unroll
-                    for (int c = 0; c < kBN; ++c) x[c] = (kv0 + c < allowed) ? x[c] : -CUDART_INF_F;
+                    for (int c = 0; c < kCols; ++c) x[c] = (kv0 + c < allowed) ? x[c] : -CUDART_INF_F;
                 }
 #pragma unroll
                 for (int u = 0; u < 8; ++u) pm[u] = x[u];
 #pragma unroll
-                for (int c = 8; c < kBN; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
-                const float mt = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
-                                       fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * sl2;
+                for (int c = 8; c < kCols; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
+                float mt = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                                 fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * sl2;
+                if constexpr (kHalves > 1) {
+                    s.red_m[b][t][hf][row] = mt;
+                    pair_sync();
+                    mt = fmaxf(mt, s.red_m[b][t][hf ^ 1][row]);
+                }
                 const bool grow = mt > m_run + kRescaleThreshold;
                 const float m_new = grow ? mt : m_run;
                 const float corr = grow ? ex2(m_run - m_new) : 1.f;
                 if (zero_owner && j + 1 == T.n_kv && row < kBN) {
-                    const int kv = kv0 + row;
+                    const int kv = j * kBN + row;
                     if (kv >= sp.context_len && kv < sp.n_pages * chunk) {
                         uint8_t* vrow = s.v[(kv_base + j) % kKvStages] + row * 128;
 #pragma unroll
@@ -472,10 +496,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float2 ps[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) ps[u] = make_float2(0.f, 0.f);
-                uint32_t pk[kBN / 2];
+                uint32_t pk[kCols / 2];
                 const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_new, -m_new);
 #pragma unroll
-                for (int c = 0; c < kBN; c += 2) {
+                for (int c = 0; c < kCols; c += 2) {
                     // exp2((s - max) * log2e / scale) on packed pairs (FFMA2 / FADD2) and MUFU
                     const float2 a = fma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
                     float2 e;
@@ -491,8 +515,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ps[(c >> 1) & 3] = add2(ps[(c >> 1) & 3], e);
                     pk[c >> 1] = pack_bf16x2(e.x, e.y);
                 }
-                // P (bf16) over the first kBN/2 columns of this S buffer
-                if (p.ablate != 5) tmem_st32(t_lane + col_s, pk); // 5: profiling, P not stored
+                // P (bf16) over the first kBN/2 columns of this S buffer (this half's share).
+                // Safe against the other half's S columns: both halves loaded their S before
+                // the max exchange above.
+                if (p.ablate != 5) {
+                    if constexpr (kCols == 64) tmem_st32(t_lane + col_s, *reinterpret_cast<uint32_t(*)[32]>(pk));
+                    else dtc::tmem_st16(t_lane + col_s + hf * (kCols / 2), *reinterpret_cast<uint32_t(*)[16]>(pk));
+                }
                 // PV_t of the previous tile must be complete before O_t is rescaled and before
                 // P_t(j) is released; waiting on it every tile also keeps pv_done at most one
                 // phase behind, so its parity wait is exact
@@ -500,13 +529,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                 if (j > 0 && __any_sync(0xffffffffu, grow)) {
                     tc_fence_after();
 #pragma unroll
-                    for (int c = 0; c < D / 32; ++c) {
+                    for (int c = 0; c < kOCols / 32; ++c) {
                         uint32_t o[32];
-                        tmem_ld32(t_lane + col_o + c * 32, o);
+                        tmem_ld32(t_lane + col_o + hf * kOCols + c * 32, o);
                         tmem_ld_wait();
 #pragma unroll
                         for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-                        tmem_st32(t_lane + col_o + c * 32, o);
+                        tmem_st32(t_lane + col_o + hf * kOCols + c * 32, o);
                     }
                 }
                 tmem_st_wait();
@@ -517,17 +546,23 @@ __global__ void __launch_bounds__(kThreads, 1)
                 l_run = l_run * corr + sum;
                 m_run = m_new;
             }
-            // epilogue: O / l -> bf16 -> global
+            // epilogue: O / l -> bf16 -> global (this half's O columns)
             mbar_wait(&s.o_ready[t], n_o & 1);
             ++n_o;
             tc_fence_after();
+            if constexpr (kHalves > 1) {
+                s.red_l[t][hf][row] = l_run;
+                pair_sync();
+                l_run += s.red_l[t][hf ^ 1][row];
+            }
             const float inv_l = 1.f / l_run;
             const int h = w.kvh * g + (row % g);
-            __nv_bfloat16* orow = out + (static_cast<size_t>(sp.query_start + tok0 + t_local) * p.n_head + h) * D;
+            __nv_bfloat16* orow =
+                out + (static_cast<size_t>(sp.query_start + tok0 + t_local) * p.n_head + h) * D + hf * kOCols;
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
+            for (int c = 0; c < kOCols / 32; ++c) {
                 uint32_t o[32];
-                tmem_ld32(t_lane + col_o + c * 32, o);
+                tmem_ld32(t_lane + col_o + hf * kOCols + c * 32, o);
                 tmem_ld_wait();
                 if (valid) {
 #pragma unroll
@@ -557,7 +592,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             ctr[3] = 0;
         }
     }
-    if (warp == 9) {
+    if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem);
     }
