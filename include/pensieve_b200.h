@@ -207,6 +207,33 @@ pb_status pb_fill_splitmix_unit(void* dst, int32_t dtype, int64_t n, uint64_t se
  * Pools: k_pool / v_pool hold n_layer pools at layer_stride bytes apart, pages of
  * page_bytes.  Moves come from pb_cache_apply_evictions (device src -> host dst) and
  * pb_cache_restore (host src -> device dst). */
+/* ---------------------------------------------------------------- pipeline event log
+ * Device-timestamped events (%globaltimer ns) of the swap / attention pipeline, kinds in the
+ * order of kvsim::EventKind (include/kvsim/event_log.hpp:14).  pb_evlog_mark enqueues a
+ * stamp on a stream (it records when that stream reached the point); a tier with a log
+ * attached stamps SWAP_IN_LAYER after each layer's pages landed and SWAP_OUT after the D2H.
+ * pb_evlog_audit restates LayerDependencyAuditor (src/event_log.cpp:90-118). */
+typedef enum pb_event_kind {
+    PB_EV_SWAP_IN_LAYER = 0,
+    PB_EV_SWAP_OUT = 1,
+    PB_EV_ATTN_START = 2,
+    PB_EV_STEP_END = 3
+} pb_event_kind;
+typedef struct pb_event_record {
+    int64_t t_ns;
+    int32_t kind;
+    int32_t layer;
+    int64_t req;
+} pb_event_record;
+typedef struct pb_event_log pb_event_log;
+pb_status pb_evlog_create(int64_t capacity, pb_event_log** out);
+void pb_evlog_destroy(pb_event_log* log);
+pb_status pb_evlog_mark(pb_event_log* log, int32_t kind, int32_t layer, int64_t req, void* stream);
+pb_status pb_evlog_read(pb_event_log* log, pb_event_record* out, int64_t cap, int64_t* n);
+pb_status pb_evlog_reset(pb_event_log* log);
+pb_status pb_evlog_audit(const pb_event_record* events, int64_t n, uint64_t* violations,
+                         uint64_t* steps);
+
 typedef struct pb_kv_tier pb_kv_tier;
 typedef struct pb_slot_move pb_slot_move; /* defined with the bookkeeping API below */
 pb_status pb_tier_create(int32_t n_layer, int32_t host_slots, int64_t page_bytes,
@@ -219,6 +246,8 @@ pb_status pb_swap_step(pb_kv_tier* tier, void* k_pool, void* v_pool, int64_t lay
                        int64_t n_in, void* compute_stream, void* copy_stream);
 pb_status pb_swap_wait_layer(pb_kv_tier* tier, int32_t layer, void* compute_stream);
 pb_status pb_swap_sync(pb_kv_tier* tier);
+/* Attach (or detach with NULL) an event log to the tier's transfers. */
+pb_status pb_tier_set_event_log(pb_kv_tier* tier, pb_event_log* log);
 
 /* ===================================================================== KV page bookkeeping
  * Two-tier slot allocator + per-conversation chunk index with the exact slot semantics of

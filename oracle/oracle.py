@@ -158,7 +158,19 @@ class Reference:
         L.ref_cache_conv_chunks.argtypes = [_P, _I64, _P, _P, _P, _I64, ctypes.POINTER(_I64)]
         L.ref_cache_dump.restype = _I64
         L.ref_cache_dump.argtypes = [_P, ctypes.c_char_p, _I64]
+        L.ref_audit_layer_deps.argtypes = [_I32, _P, _P, _P, ctypes.POINTER(_U64), ctypes.POINTER(_U64)]
         self.L = L
+
+    # ---- event log -------------------------------------------------------------------
+    def audit_layer_deps(self, kinds, layers, times_s):
+        """kvsim::LayerDependencyAuditor fed these events in order -> (violations, steps)."""
+        k = np.ascontiguousarray(kinds, np.int32)
+        ly = np.ascontiguousarray(layers, np.int32)
+        t = np.ascontiguousarray(times_s, np.float64)
+        v, st = _U64(), _U64()
+        self.L.ref_audit_layer_deps(len(k), k.ctypes.data, ly.ctypes.data, t.ctypes.data, ctypes.byref(v),
+                                    ctypes.byref(st))
+        return int(v.value), int(st.value)
 
     # ---- attention -------------------------------------------------------------------
     def store(self, chunk, n_kv, hs, n_slots, keys=None, values=None):

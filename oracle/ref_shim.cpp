@@ -8,6 +8,7 @@
 // copied: this file only marshals plain arrays into the reference's own types and maps its
 // exception classes (proj/include/kvsim/errors.hpp) onto PB_* status codes.
 #include "kvsim/attention.hpp"
+#include "kvsim/event_log.hpp"
 #include "kvsim/errors.hpp"
 #include "kvsim/model_config.hpp"
 #include "kvsim/paged_kv_cache.hpp"
@@ -354,6 +355,23 @@ int64_t ref_cache_dump(void* h, char* buf, int64_t cap) {
         buf[n] = '\0';
     }
     return static_cast<int64_t>(s.size());
+}
+
+// ------------------------------------------------------------------------ event log
+// The reference's LayerDependencyAuditor over n events (times in seconds, kinds in
+// kvsim::EventKind order), fed in the given order.
+void ref_audit_layer_deps(int n, const int* kinds, const int* layers, const double* times,
+                          unsigned long long* violations, unsigned long long* steps) {
+    LayerDependencyAuditor a;
+    for (int i = 0; i < n; ++i) {
+        LogEvent ev;
+        ev.t = times[i];
+        ev.kind = static_cast<EventKind>(kinds[i]);
+        ev.layer = layers[i];
+        a.on_event(ev);
+    }
+    *violations = a.violations();
+    *steps = a.steps_checked();
 }
 
 } // extern "C"

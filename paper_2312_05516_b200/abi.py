@@ -475,6 +475,13 @@ _TIER_SIGS = {
     "pb_swap_step": (_I32, [_P, _P, _P, _I64, _P, _I64, _P, _I64, _P, _P]),
     "pb_swap_wait_layer": (_I32, [_P, _I32, _P]),
     "pb_swap_sync": (_I32, [_P]),
+    "pb_tier_set_event_log": (_I32, [_P, _P]),
+    "pb_evlog_create": (_I32, [_I64, ctypes.POINTER(_P)]),
+    "pb_evlog_destroy": (None, [_P]),
+    "pb_evlog_mark": (_I32, [_P, _I32, _I32, _I64, _P]),
+    "pb_evlog_read": (_I32, [_P, _P, _I64, ctypes.POINTER(_I64)]),
+    "pb_evlog_reset": (_I32, [_P]),
+    "pb_evlog_audit": (_I32, [_P, _I64, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]),
 }
 for _name, (_res, _args) in _TIER_SIGS.items():
     _f = getattr(lib, _name)
@@ -488,6 +495,47 @@ def _moves_array(moves):
     for i, (c, s, d) in enumerate(moves):
         arr[i].chunk, arr[i].src_slot, arr[i].dst_slot = c, s, d
     return arr
+
+
+PB_EV_SWAP_IN_LAYER, PB_EV_SWAP_OUT, PB_EV_ATTN_START, PB_EV_STEP_END = 0, 1, 2, 3
+EVENT_DTYPE = np.dtype([("t_ns", np.int64), ("kind", np.int32), ("layer", np.int32), ("req", np.int64)])
+
+
+def audit_events(events: np.ndarray):
+    """pb_evlog_audit: LayerDependencyAuditor (src/event_log.cpp:90-118) over records of
+    EVENT_DTYPE.  Returns (violations, steps)."""
+    ev = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
+    v, st = ctypes.c_uint64(), ctypes.c_uint64()
+    check(lib.pb_evlog_audit(ev.ctypes.data if len(ev) else None, len(ev), ctypes.byref(v), ctypes.byref(st)))
+    return int(v.value), int(st.value)
+
+
+class EventLog:
+    """pb_event_log: device-timestamped pipeline events."""
+
+    def __init__(self, capacity: int = 1 << 16):
+        h = _P()
+        check(lib.pb_evlog_create(capacity, ctypes.byref(h)))
+        self._h = h
+        self.capacity = capacity
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib.pb_evlog_destroy(h)
+            self._h = None
+
+    def mark(self, kind: int, layer: int = -1, req: int = -1, stream: Optional[int] = None) -> None:
+        check(lib.pb_evlog_mark(self._h, kind, layer, req, stream))
+
+    def read(self) -> np.ndarray:
+        n = ctypes.c_int64()
+        out = np.zeros(self.capacity, dtype=EVENT_DTYPE)
+        check(lib.pb_evlog_read(self._h, out.ctypes.data, self.capacity, ctypes.byref(n)))
+        return out[: n.value]
+
+    def reset(self) -> None:
+        check(lib.pb_evlog_reset(self._h))
 
 
 class KvTier:
@@ -520,6 +568,10 @@ class KvTier:
         om, im = _moves_array(out_moves), _moves_array(in_moves)
         check(lib.pb_swap_step(self._h, k_pool, v_pool, layer_stride, om, len(out_moves), im, len(in_moves),
                                compute_stream, copy_stream))
+
+    def set_event_log(self, log: Optional["EventLog"]) -> None:
+        self._log = log
+        check(lib.pb_tier_set_event_log(self._h, log._h if log is not None else None))
 
     def wait_layer(self, layer: int, compute_stream: Optional[int] = None) -> None:
         check(lib.pb_swap_wait_layer(self._h, layer, compute_stream))

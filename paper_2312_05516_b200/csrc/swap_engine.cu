@@ -157,6 +157,7 @@ struct pb_kv_tier {
     cudaEvent_t d2h_done = nullptr;
     int mode_zc = 0, mode_duplex = 0;
     int layer_block = 1;           // staged swap-in: layers per H2D piece (larger pieces, coarser events)
+    pb_event_log* log = nullptr;   // optional: stamps SWAP_IN_LAYER / SWAP_OUT
     cudaEvent_t gathered = nullptr, done = nullptr;
     std::vector<cudaEvent_t> layer_ready;
     bool any_in = false;
@@ -306,6 +307,10 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
                 cuda_check(cudaGetLastError(), "swap scatter");
                 count_launch();
             }
+            if (T->log && n_in > 0) {
+                const pb_status r = pb_evlog_mark(T->log, PB_EV_SWAP_IN_LAYER, l, -1, xs);
+                if (r != PB_OK) fail(r, "swap-in stamp");
+            }
             cuda_check(cudaEventRecord(T->layer_ready[static_cast<size_t>(l)], xs), "event record");
         }
         // 3. swap-out D2H: behind the swap-ins on the copy stream (the reference's order, no
@@ -325,6 +330,10 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
                 sz.push_back(static_cast<size_t>(T->chunk_bytes()));
             }
             copy_batch(dst, src, sz, os);
+            if (T->log) {
+                const pb_status r = pb_evlog_mark(T->log, PB_EV_SWAP_OUT, -1, -1, os);
+                if (r != PB_OK) fail(r, "swap-out stamp");
+            }
         }
         if (T->mode_duplex) {
             cuda_check(cudaEventRecord(T->d2h_done, os), "event record");
@@ -339,6 +348,13 @@ pb_status pb_swap_wait_layer(pb_kv_tier* T, int32_t layer, void* compute_stream)
         if (!T || layer < 0 || layer >= T->n_layer) fail(PB_ERR_DIMENSION_MISMATCH, "layer out of range");
         cuda_check(cudaStreamWaitEvent(as_stream(compute_stream), T->layer_ready[static_cast<size_t>(layer)], 0),
                    "stream wait");
+    });
+}
+
+pb_status pb_tier_set_event_log(pb_kv_tier* T, pb_event_log* log) {
+    return guarded([&] {
+        if (!T) fail(PB_ERR_ERROR, "null tier");
+        T->log = log;
     });
 }
 
