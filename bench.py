@@ -494,6 +494,29 @@ def bench_config5(args):
 
     attn_only_ms = timed_loop(attn_only)
     swap_only_ms = timed_loop(swap_only)
+
+    # untimed audit pass: device-stamped swap-in completions vs attention starts per layer,
+    # checked by the LayerDependencyAuditor restatement (pb_evlog_audit)
+    log = abi.EventLog(1 << 16)
+    tier.set_event_log(log)
+
+    def audited(i):
+        p, pl = steps[i], plans[i]
+        tier.step(k.data_ptr(), v.data_ptr(), layer_stride, p.out_moves, p.in_moves, cs.cuda_stream, xs.cuda_stream)
+        pl.upload(cs.cuda_stream)
+        for l in range(n_layer):
+            tier.wait_layer(l, cs.cuda_stream)
+            log.mark(abi.PB_EV_ATTN_START, l, -1, cs.cuda_stream)
+            pl.run(q.data_ptr(), k.data_ptr() + l * layer_stride, v.data_ptr() + l * layer_stride, out.data_ptr(),
+                   wsb.data_ptr(), cs.cuda_stream)
+        log.mark(abi.PB_EV_STEP_END, -1, -1, cs.cuda_stream)
+
+    for s_ in range(args.steps):
+        audited(args.warmup + s_)
+    torch.cuda.synchronize()
+    events = log.read()
+    tier.set_event_log(None)
+    violations, audited_steps = abi.audit_events(events, per_step=True)
     timed = steps[args.warmup:args.warmup + args.steps]
     attn_bytes = sum(pl.stats()["bytes"] for pl in plans[args.warmup:args.warmup + args.steps]) * n_layer
     attn_flops = sum(pl.stats()["flops"] for pl in plans[args.warmup:args.warmup + args.steps]) * n_layer
@@ -525,6 +548,9 @@ def bench_config5(args):
         "roofline": {"bound": "hbm", "achieved": value, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": value / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_src,
                      "tflops": attn_flops / (total_ms / 1e3) / 1e12},
+        "pipeline_audit": {"violations": violations, "steps": audited_steps,
+                           "swap_in_layer_events": int((events["kind"] == abi.PB_EV_SWAP_IN_LAYER).sum()),
+                           "attn_start_events": int((events["kind"] == abi.PB_EV_ATTN_START).sum())},
         "parts_ms_per_step": {"attention_only": attn_only_ms, "swap_only": swap_only_ms,
                               "both": total_ms / args.steps},
         "swap": {"chunks_in": n_in, "chunks_out": n_out, "bytes": swap_bytes,

@@ -233,6 +233,10 @@ pb_status pb_evlog_read(pb_event_log* log, pb_event_record* out, int64_t cap, in
 pb_status pb_evlog_reset(pb_event_log* log);
 pb_status pb_evlog_audit(const pb_event_record* events, int64_t n, uint64_t* violations,
                          uint64_t* steps);
+/* Per-step form: readiness of a layer = latest SWAP_IN_LAYER of that layer anywhere in the
+ * step (events between STEP_ENDs), so an attention stamped before its swap-in is flagged. */
+pb_status pb_evlog_audit_steps(const pb_event_record* events, int64_t n, uint64_t* violations,
+                               uint64_t* steps);
 
 typedef struct pb_kv_tier pb_kv_tier;
 typedef struct pb_slot_move pb_slot_move; /* defined with the bookkeeping API below */

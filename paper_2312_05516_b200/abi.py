@@ -482,6 +482,7 @@ _TIER_SIGS = {
     "pb_evlog_read": (_I32, [_P, _P, _I64, ctypes.POINTER(_I64)]),
     "pb_evlog_reset": (_I32, [_P]),
     "pb_evlog_audit": (_I32, [_P, _I64, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]),
+    "pb_evlog_audit_steps": (_I32, [_P, _I64, ctypes.POINTER(ctypes.c_uint64), ctypes.POINTER(ctypes.c_uint64)]),
 }
 for _name, (_res, _args) in _TIER_SIGS.items():
     _f = getattr(lib, _name)
@@ -501,12 +502,13 @@ PB_EV_SWAP_IN_LAYER, PB_EV_SWAP_OUT, PB_EV_ATTN_START, PB_EV_STEP_END = 0, 1, 2,
 EVENT_DTYPE = np.dtype([("t_ns", np.int64), ("kind", np.int32), ("layer", np.int32), ("req", np.int64)])
 
 
-def audit_events(events: np.ndarray):
+def audit_events(events: np.ndarray, per_step: bool = False):
     """pb_evlog_audit: LayerDependencyAuditor (src/event_log.cpp:90-118) over records of
-    EVENT_DTYPE.  Returns (violations, steps)."""
+    EVENT_DTYPE (per_step: pb_evlog_audit_steps).  Returns (violations, steps)."""
     ev = np.ascontiguousarray(events, dtype=EVENT_DTYPE)
     v, st = ctypes.c_uint64(), ctypes.c_uint64()
-    check(lib.pb_evlog_audit(ev.ctypes.data if len(ev) else None, len(ev), ctypes.byref(v), ctypes.byref(st)))
+    fn = lib.pb_evlog_audit_steps if per_step else lib.pb_evlog_audit
+    check(fn(ev.ctypes.data if len(ev) else None, len(ev), ctypes.byref(v), ctypes.byref(st)))
     return int(v.value), int(st.value)
 
 

@@ -137,4 +137,43 @@ pb_status pb_evlog_audit(const pb_event_record* ev, int64_t n, uint64_t* violati
     });
 }
 
+// The same rule per step instead of streaming: the events between two STEP_ENDs (in log
+// order) form a step; a layer's readiness is the latest SWAP_IN_LAYER of that layer anywhere
+// in the step, and every ATTN_START of the layer in the step must be at or after it (1 ns
+// tolerance).  On a device-stamped log (stamp order = time order) the streaming auditor can
+// only see an attention that was stamped before its swap-in as "not yet ready"; this form
+// flags it.
+pb_status pb_evlog_audit_steps(const pb_event_record* ev, int64_t n, uint64_t* violations, uint64_t* steps) {
+    return guarded([&] {
+        if ((!ev && n > 0) || !violations || !steps) fail(PB_ERR_ERROR, "null argument");
+        uint64_t v = 0, st = 0;
+        int64_t begin = 0;
+        std::vector<int64_t> ready;
+        for (int64_t end = 0; end <= n; ++end) {
+            if (end < n && ev[end].kind != PB_EV_STEP_END) continue;
+            ready.clear();
+            for (int64_t i = begin; i < end; ++i) {
+                const pb_event_record& e = ev[i];
+                if (e.kind != PB_EV_SWAP_IN_LAYER) continue;
+                if (e.layer < 0) {
+                    ++v;
+                    continue;
+                }
+                if (static_cast<size_t>(e.layer) >= ready.size()) ready.resize(static_cast<size_t>(e.layer) + 1, -1);
+                ready[static_cast<size_t>(e.layer)] = std::max(ready[static_cast<size_t>(e.layer)], e.t_ns);
+            }
+            for (int64_t i = begin; i < end; ++i) {
+                const pb_event_record& e = ev[i];
+                if (e.kind != PB_EV_ATTN_START || e.layer < 0 || static_cast<size_t>(e.layer) >= ready.size()) continue;
+                const int64_t r = ready[static_cast<size_t>(e.layer)];
+                if (r >= 0 && e.t_ns < r - 1) ++v;
+            }
+            if (end < n) ++st;
+            begin = end + 1;
+        }
+        *violations = v;
+        *steps = st;
+    });
+}
+
 } // extern "C"

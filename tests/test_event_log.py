@@ -80,15 +80,25 @@ def test_swap_pipeline_audit_on_gpu(cuda):
     ev = log.read()
     assert (ev["kind"] == PB_EV_SWAP_IN_LAYER).sum() == 3 * n_layer
     assert audit_events(ev) == (0, 3)
-    # the same step without waiting for the last layer: its attention stamp lands before
-    # that layer's (large) swap-in completes
+    assert audit_events(ev, per_step=True) == (0, 3)
+    # an attention of the last layer stamped before the step's swap-in was even issued: the
+    # per-step audit flags it (the streaming form sees a layer that is not "ready" yet)
     log.reset()
-    big_in = [(i, i % 32, 2 * (i % 32)) for i in range(32)]
-    with torch.cuda.stream(cs):
-        torch.cuda._sleep(200000)  # delays the step's transfers (they follow cs's slot upload)
-    tier.step(k.data_ptr(), v.data_ptr(), layer_stride, [], big_in, cs.cuda_stream, xs.cuda_stream)
-    log.mark(PB_EV_ATTN_START, n_layer - 1, -1, torch.cuda.Stream().cuda_stream)
-    torch.cuda.synchronize()
+    log.mark(PB_EV_ATTN_START, n_layer - 1, -1, cs.cuda_stream)
+    tier.step(k.data_ptr(), v.data_ptr(), layer_stride, [], moves_in, cs.cuda_stream, xs.cuda_stream)
+    for l in range(n_layer - 1):
+        tier.wait_layer(l, cs.cuda_stream)
+        log.mark(PB_EV_ATTN_START, l, -1, cs.cuda_stream)
+    tier.wait_layer(n_layer - 1, cs.cuda_stream)
     log.mark(PB_EV_STEP_END, -1, -1, cs.cuda_stream)
     torch.cuda.synchronize()
-    assert audit_events(log.read())[0] >= 1
+    bad = log.read()
+    assert audit_events(bad, per_step=True) == (1, 1)
+    assert audit_events(bad) == (0, 1)
+
+
+def test_per_step_audit_cases():
+    ev = _ev([(0.002, PB_EV_ATTN_START, 0), (0.003, PB_EV_SWAP_IN_LAYER, 0), (0.004, PB_EV_STEP_END, -1),
+              (0.005, PB_EV_SWAP_IN_LAYER, 0), (0.006, PB_EV_ATTN_START, 0), (0.007, PB_EV_STEP_END, -1)])
+    assert audit_events(ev, per_step=True) == (1, 2)
+    assert audit_events(ev) == (0, 2)
