@@ -72,6 +72,9 @@ constexpr int kLaunchRegs = (65536 / (128 * ((PB_SPLIT ? 4 : 2) + 1))) / 8 * 8;
 static_assert((PB_REG_HI - kLaunchRegs) * (PB_SPLIT ? 4 : 2) <= (kLaunchRegs - PB_REG_LO),
               "setmaxnreg budget exceeds the launch register allocation");
 constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max grows by > 2^8
+#ifndef PB_MMA_POLL
+#define PB_MMA_POLL 0   // 1: MMA warp issues S(j+1) / PV_A(j) / PV_B(j) in readiness order
+#endif
 #ifndef PB_POLY_EVERY
 #define PB_POLY_EVERY 0 // one exp2 pair in N on the FMA pipe; 0 = all on MUFU (measured fastest, see profiles/)
 #endif
@@ -356,8 +359,42 @@ __global__ void __launch_bounds__(kThreads, 1)
                 };
                 // S runs one kv tile ahead of PV: S(j+1) is computed while the softmax groups
                 // turn S(j) into P(j) (two S buffers per group)
+                // S(j) for both groups of the first kv tile needs K(0) before anything else
                 issue_s(0);
                 for (int j = 0; j < T.n_kv; ++j) {
+#if PB_MMA_POLL
+                    // issue S(j+1), PV_A(j), PV_B(j) in whatever order their inputs become ready
+                    bool s_next = j + 1 >= T.n_kv;
+                    bool pv[2] = {j >= T.ntiles[0], j >= T.ntiles[1]};
+                    bool v_in = false;
+                    const uint64_t vd = umma_desc_sw128(smem_u32(s.v[vst]), kKvHalf, 1024);
+                    while (!(s_next && pv[0] && pv[1])) {
+                        if (!s_next && mbar_try_wait(smem_u32(&s.k_full[kst]), kph)) {
+                            issue_s(j + 1);
+                            s_next = true;
+                        }
+                        if (!v_in) v_in = mbar_try_wait(smem_u32(&s.v_full[vst]), vph);
+                        if (!v_in) continue;
+                        for (int t = 0; t < 2; ++t) {
+                            if (pv[t] || !mbar_try_wait(smem_u32(&s.p_full[t]), n_p[t] & 1)) continue;
+                            if (j == 0) {
+                                mbar_wait(&s.o_empty[t], (n_oe[t] & 1) ^ 1);
+                                ++n_oe[t];
+                            }
+                            ++n_p[t];
+                            tc_fence_after();
+                            const uint32_t pcol = t * 128 + (c_p[t] & 1) * kBN;
+#pragma unroll
+                            for (int kk = 0; kk < kBN / 16; ++kk)
+                                umma_bf16_ts(tmem + kColO + t * 128, tmem + pcol + kk * 8, vd + kk * (2048 >> 4),
+                                             idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+                            ++c_p[t];
+                            umma_commit(&s.pv_done[t]);
+                            if (j + 1 == T.ntiles[t]) umma_commit(&s.o_ready[t]);
+                            pv[t] = true;
+                        }
+                    }
+#else
                     if (j + 1 < T.n_kv) issue_s(j + 1);
                     mbar_wait(&s.v_full[vst], vph);
                     const uint64_t vd = umma_desc_sw128(smem_u32(s.v[vst]), kKvHalf, 1024);
@@ -379,6 +416,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                         umma_commit(&s.pv_done[t]);
                         if (j + 1 == T.ntiles[t]) umma_commit(&s.o_ready[t]);
                     }
+#endif
                     umma_commit(&s.v_empty[vst]);
                     if (++vst == kKvStages) { vst = 0; vph ^= 1; }
                 }

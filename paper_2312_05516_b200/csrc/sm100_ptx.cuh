@@ -124,18 +124,6 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&r)[32
         : "memory");
 }
 __device__ __forceinline__ void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
-// wait::ld that also "redefines" r, so the compiler cannot schedule a use of r above the wait
-__device__ __forceinline__ void tmem_ld_wait_dep(uint32_t (&r)[32]) {
-    asm volatile(
-        "tcgen05.wait::ld.sync.aligned;"
-        : "+r"(r[0]), "+r"(r[1]), "+r"(r[2]), "+r"(r[3]), "+r"(r[4]), "+r"(r[5]), "+r"(r[6]), "+r"(r[7]),
-          "+r"(r[8]), "+r"(r[9]), "+r"(r[10]), "+r"(r[11]), "+r"(r[12]), "+r"(r[13]), "+r"(r[14]),
-          "+r"(r[15]), "+r"(r[16]), "+r"(r[17]), "+r"(r[18]), "+r"(r[19]), "+r"(r[20]), "+r"(r[21]),
-          "+r"(r[22]), "+r"(r[23]), "+r"(r[24]), "+r"(r[25]), "+r"(r[26]), "+r"(r[27]), "+r"(r[28]),
-          "+r"(r[29]), "+r"(r[30]), "+r"(r[31])
-        :
-        : "memory");
-}
 __device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
 // ---------------------------------------------------------------- UMMA
@@ -191,21 +179,6 @@ __device__ __forceinline__ float ex2(float x) {
     return y;
 }
 
-// 2^x on the FMA/ALU pipes (for x <= ~8): round-to-nearest integer j via the 1.5*2^23
-// magic add, cubic fit of 2^f on [-0.5, 0.5] (max rel. err 1.8e-4, far below bf16's 3.9e-3),
-// exponent added as integer bits.  x < -126 (incl. masked -inf) returns exactly 0; the
-// clamp keeps the integer exponent add from wrapping into the sign bit.
-__device__ __forceinline__ float exp2_poly3(float x) {
-    const float xc = fmaxf(x, -126.f);
-    const float r = xc + 12582912.f;
-    const float f = xc - (r - 12582912.f);
-    float p = fmaf(0.05324155f, f, 0.24228422f);
-    p = fmaf(p, f, 0.69354963f);
-    p = fmaf(p, f, 0.9999545f);
-    const float y = __int_as_float(__float_as_int(p) + (__float_as_int(r) << 23));
-    return x < -126.f ? 0.f : y;
-}
-
 // ---- packed fp32x2 math (sm_100: FFMA2 / FADD2 / FMUL2 issue two lanes per instruction)
 __device__ __forceinline__ uint64_t f2_bits(float2 v) { return *reinterpret_cast<uint64_t*>(&v); }
 __device__ __forceinline__ float2 bits_f2(uint64_t v) { return *reinterpret_cast<float2*>(&v); }
@@ -223,24 +196,6 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) {
     uint64_t d;
     asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(d) : "l"(f2_bits(a)), "l"(f2_bits(b)));
     return bits_f2(d);
-}
-
-// exp2_poly3 on a pair, with packed fp32x2 arithmetic
-__device__ __forceinline__ float2 exp2_poly3_x2(float2 x) {
-    const float2 xc = make_float2(fmaxf(x.x, -126.f), fmaxf(x.y, -126.f));
-    const float2 magic = make_float2(12582912.f, 12582912.f);
-    const float2 r = add2(xc, magic);
-    const float2 rounded = add2(r, make_float2(-12582912.f, -12582912.f));
-    const float2 f = fma2(rounded, make_float2(-1.f, -1.f), xc); // xc - round(xc) in [-0.5, 0.5]
-    float2 p = fma2(make_float2(0.05324155f, 0.05324155f), f, make_float2(0.24228422f, 0.24228422f));
-    p = fma2(p, f, make_float2(0.69354963f, 0.69354963f));
-    p = fma2(p, f, make_float2(0.9999545f, 0.9999545f));
-    float2 y;
-    y.x = __int_as_float(__float_as_int(p.x) + (__float_as_int(r.x) << 23));
-    y.y = __int_as_float(__float_as_int(p.y) + (__float_as_int(r.y) << 23));
-    y.x = x.x < -126.f ? 0.f : y.x;
-    y.y = x.y < -126.f ? 0.f : y.y;
-    return y;
 }
 
 // Cheaper 2^x on a pair for x <= 0: clamp at -127, round with the 1.5*2^23 magic add, cubic
