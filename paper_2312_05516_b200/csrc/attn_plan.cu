@@ -70,7 +70,10 @@ int sm_count() {
         int dev = 0;
         cudaGetDevice(&dev);
         cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
+        if (n <= 0) {
+            cudaGetLastError(); // no device (host-only plan building): B200's count
+            n = 148;
+        }
     }
     return n;
 }
@@ -144,9 +147,24 @@ void build_work(pb_attn_plan& P) {
         const char* e = std::getenv("PB_DEC_UNITS");
         return e ? std::max<int64_t>(1, std::atoll(e)) : static_cast<int64_t>(kDecodeUnitsTargetTc);
     }();
-    const int split_pages =
-        dec_tc ? static_cast<int>(std::max<int64_t>(16, std::min<int64_t>(128, decode_pages / units_tc)))
-               : static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(64, decode_pages / kDecodeUnitsTarget)));
+    int64_t decode_pairs = 0;
+    for (const SpanDev& sp : P.spans)
+        if (sp.query_len == 1) decode_pairs += s.n_kv_head;
+    // tcgen05 decode: a split span costs a partial write, an atomic ticket and a merge, which
+    // measured slower than whole spans as soon as there is at least one (span, kv head) pair
+    // per CTA (cfg3: 95% -> 99% of HBM; the config-5 steps: 52 -> 40 us); with fewer pairs,
+    // split to ~1.5 units per CTA (>= 16 pages each).  PB_DEC_UNITS (profiling) forces a
+    // unit-count target instead.
+    const int64_t sms = sm_count();
+    int split_pages;
+    if (dec_tc && std::getenv("PB_DEC_UNITS"))
+        split_pages = static_cast<int>(std::max<int64_t>(16, std::min<int64_t>(128, decode_pages / units_tc)));
+    else if (dec_tc)
+        split_pages = decode_pairs >= sms
+                          ? (1 << 24) // no split
+                          : static_cast<int>(std::max<int64_t>(16, (2 * decode_pages + 3 * sms - 1) / (3 * sms)));
+    else
+        split_pages = static_cast<int>(std::max<int64_t>(8, std::min<int64_t>(64, decode_pages / kDecodeUnitsTarget)));
     for (int32_t si = 0; si < static_cast<int32_t>(P.spans.size()); ++si) {
         const SpanDev& sp = P.spans[si];
         if (sp.query_len == 0) continue;

@@ -179,8 +179,12 @@ def test_gqa_duplicated_kv_equals_mha_on_gpu(gh, cuda):
     assert ok, err
 
 
-def test_split_decode_matches_unsplit(gh):
-    w = config(3)
+@pytest.mark.parametrize("n_kv", [10, 1])
+def test_split_decode_matches_unsplit(gh, n_kv):
+    """Few (span, kv head) pairs with long contexts: the plan splits them across CTAs and
+    merges the partials; the result matches the unsplit run (and the oracle, elsewhere)."""
+    rng = SplitMix64(60 + n_kv)
+    w = random_instance(rng, 4 * n_kv, n_kv, 128, 16, PB_BF16, 12, 6000, all_decode=True)
     q, k, v = gh.device_inputs(w)
     a, pa = gh.run_plan(w, q, k, v)
     b, pb_ = gh.run_plan(w, q, k, v, flags=abi.PB_PLAN_NO_SPLIT)
