@@ -148,10 +148,16 @@ struct pb_kv_tier {
     int32_t n_layer = 0, host_slots = 0, max_chunks = 0;
     int64_t page_bytes = 0;
     uint8_t* host = nullptr;       // pinned [host_slot][layer][K|V][page]
-    uint8_t* stage_out = nullptr;  // device [chunk][layer][K|V][page]
-    uint8_t* stage_in = nullptr;   // device [layer][chunk][K|V][page]
-    int32_t* d_slots = nullptr;    // device: [out src slots | in dst slots | in host src slots]
-    int32_t* h_slots = nullptr;    // pinned staging for the slot lists
+    // per-step buffers, double-buffered by step parity so step s+1 can be issued while step
+    // s's transfers (the swap-out D2H above all) are still running
+    uint8_t* stage_out[2] = {};    // device [chunk][layer][K|V][page]
+    uint8_t* stage_in[2] = {};     // device [layer block][chunk][layers][K|V][page]
+    int32_t* d_slots[2] = {};      // device: [out src slots | in dst slots | in host src slots]
+    int32_t* h_slots[2] = {};      // pinned staging for the slot lists
+    cudaEvent_t done_p[2] = {};    // step with this parity fully done (transfers + D2H)
+    cudaEvent_t d2h_prev = nullptr; // last issued swap-out D2H (host-slot RAW for swap-ins)
+    int par = 0;
+    bool have_prev = false;
     const uint8_t* host_dev = nullptr; // device alias of the pinned tier (zero-copy swap-in)
     cudaStream_t d2h = nullptr;    // duplex mode: swap-out D2H on its own stream
     cudaEvent_t d2h_done = nullptr;
@@ -184,14 +190,19 @@ pb_status pb_tier_create(int32_t n_layer, int32_t host_slots, int64_t page_bytes
             fail(PB_ERR_INSUFFICIENT_HOST_MEMORY, "pinned host tier allocation failed");
         }
         const size_t stage_bytes = static_cast<size_t>(max_chunks_per_step) * T->chunk_bytes();
-        if (cudaMalloc(&T->stage_out, stage_bytes) != cudaSuccess || cudaMalloc(&T->stage_in, stage_bytes) != cudaSuccess) {
-            cudaGetLastError();
-            fail(PB_ERR_INSUFFICIENT_DEVICE_MEMORY, "swap staging allocation failed");
+        for (int b = 0; b < 2; ++b) {
+            if (cudaMalloc(&T->stage_out[b], stage_bytes) != cudaSuccess ||
+                cudaMalloc(&T->stage_in[b], stage_bytes) != cudaSuccess) {
+                cudaGetLastError();
+                fail(PB_ERR_INSUFFICIENT_DEVICE_MEMORY, "swap staging allocation failed");
+            }
+            cuda_check(cudaMalloc(&T->d_slots[b], sizeof(int32_t) * 3 * max_chunks_per_step), "cudaMalloc(slots)");
+            cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&T->h_slots[b]), sizeof(int32_t) * 3 * max_chunks_per_step,
+                                     cudaHostAllocPortable),
+                       "cudaHostAlloc(slots)");
+            cuda_check(cudaEventCreateWithFlags(&T->done_p[b], cudaEventDisableTiming), "event");
         }
-        cuda_check(cudaMalloc(&T->d_slots, sizeof(int32_t) * 3 * max_chunks_per_step), "cudaMalloc(slots)");
-        cuda_check(cudaHostAlloc(reinterpret_cast<void**>(&T->h_slots), sizeof(int32_t) * 3 * max_chunks_per_step,
-                                 cudaHostAllocPortable),
-                   "cudaHostAlloc(slots)");
+        cuda_check(cudaEventCreateWithFlags(&T->d2h_prev, cudaEventDisableTiming), "event");
         void* hd = nullptr;
         if (cudaHostGetDevicePointer(&hd, T->host, 0) == cudaSuccess) T->host_dev = static_cast<const uint8_t*>(hd);
         else cudaGetLastError();
@@ -216,11 +227,18 @@ pb_status pb_tier_create(int32_t n_layer, int32_t host_slots, int64_t page_bytes
 void pb_tier_destroy(pb_kv_tier* T) {
     if (!T) return;
     if (T->done) cudaEventSynchronize(T->done);
+    for (int b = 0; b < 2; ++b) {
+        if (T->done_p[b]) {
+            cudaEventSynchronize(T->done_p[b]);
+            cudaEventDestroy(T->done_p[b]);
+        }
+        cudaFree(T->stage_out[b]);
+        cudaFree(T->stage_in[b]);
+        cudaFree(T->d_slots[b]);
+        cudaFreeHost(T->h_slots[b]);
+    }
+    if (T->d2h_prev) cudaEventDestroy(T->d2h_prev);
     cudaFreeHost(T->host);
-    cudaFree(T->stage_out);
-    cudaFree(T->stage_in);
-    cudaFree(T->d_slots);
-    cudaFreeHost(T->h_slots);
     if (T->d2h) {
         cudaStreamSynchronize(T->d2h);
         cudaStreamDestroy(T->d2h);
@@ -250,14 +268,30 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
             if (in_moves[i].src_slot < 0 || in_moves[i].src_slot >= T->host_slots || in_moves[i].dst_slot < 0)
                 fail(PB_ERR_ERROR, "swap-in move needs a host source and a device destination slot");
         cudaStream_t cs = as_stream(compute_stream), xs = as_stream(copy_stream);
-        // the previous step's transfers must be done before the slot staging is rewritten
-        cuda_check(cudaEventSynchronize(T->done), "swap step ordering");
-        for (int64_t i = 0; i < n_out; ++i) T->h_slots[i] = out_moves[i].src_slot;
-        for (int64_t i = 0; i < n_in; ++i) T->h_slots[T->max_chunks + i] = in_moves[i].dst_slot;
-        for (int64_t i = 0; i < n_in; ++i) T->h_slots[2 * T->max_chunks + i] = in_moves[i].src_slot;
-        cuda_check(cudaMemcpyAsync(T->d_slots, T->h_slots, sizeof(int32_t) * 3 * T->max_chunks,
-                                   cudaMemcpyHostToDevice, cs),
+        // this step's buffers were last used two steps ago: only that step must be done
+        const int par = T->par;
+        T->par ^= 1;
+        cuda_check(cudaEventSynchronize(T->done_p[par]), "swap step ordering");
+        int32_t* h_slots = T->h_slots[par];
+        int32_t* d_slots = T->d_slots[par];
+        uint8_t* stage_out = T->stage_out[par];
+        uint8_t* stage_in = T->stage_in[par];
+        for (int64_t i = 0; i < n_out; ++i) h_slots[i] = out_moves[i].src_slot;
+        for (int64_t i = 0; i < n_in; ++i) h_slots[T->max_chunks + i] = in_moves[i].dst_slot;
+        for (int64_t i = 0; i < n_in; ++i) h_slots[2 * T->max_chunks + i] = in_moves[i].src_slot;
+        cuda_check(cudaMemcpyAsync(d_slots, h_slots, sizeof(int32_t) * 3 * T->max_chunks, cudaMemcpyHostToDevice, cs),
                    "slot upload");
+        // host-slot hazards: a swap-in may read a host slot the previous step's swap-out wrote
+        // (RAW: the swap-ins wait for that D2H), and restore frees host slots at once, so this
+        // step's swap-out may overwrite a slot one of this step's swap-ins reads (WAR: then the
+        // D2H waits for the swap-ins, the reference's order, src/swap_engine.cpp:50-53)
+        bool war = false;
+        for (int64_t i = 0; i < n_out && !war; ++i)
+            for (int64_t j = 0; j < n_in; ++j)
+                if (out_moves[i].dst_slot == in_moves[j].src_slot) {
+                    war = true;
+                    break;
+                }
         const int64_t pb = T->page_bytes;
         auto* kp = static_cast<uint8_t*>(k_pool);
         auto* vp = static_cast<uint8_t*>(v_pool);
@@ -265,13 +299,14 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         if (n_out > 0) {
             const int64_t jobs = n_out * T->n_layer * 2;
             const int grid = static_cast<int>(std::min<int64_t>(jobs, n_sms() * 8));
-            swap_gather_kernel<<<grid, 256, 0, cs>>>(kp, vp, layer_stride, pb, T->d_slots, static_cast<int32_t>(n_out),
-                                                     T->n_layer, T->stage_out);
+            swap_gather_kernel<<<grid, 256, 0, cs>>>(kp, vp, layer_stride, pb, d_slots, static_cast<int32_t>(n_out),
+                                                     T->n_layer, stage_out);
             cuda_check(cudaGetLastError(), "swap gather");
             count_launch();
         }
         cuda_check(cudaEventRecord(T->gathered, cs), "event record");
         cuda_check(cudaStreamWaitEvent(xs, T->gathered, 0), "stream wait");
+        if (T->have_prev && n_in > 0) cuda_check(cudaStreamWaitEvent(xs, T->d2h_prev, 0), "stream wait");
         // 2. swap-in, layer by layer: H2D (batched) into staging, scatter, per-layer event
         T->any_in = n_in > 0;
         std::vector<void*> dst, src;
@@ -281,8 +316,8 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
                 const int64_t vecs = n_in * 2 * (pb / 16);
                 const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((vecs + 1023) / 1024, n_sms() * 4)));
                 swap_in_zc_layer_kernel<<<grid, 256, 0, xs>>>(T->host_dev, T->chunk_bytes(), static_cast<int64_t>(l) * 2 * pb,
-                                                              pb, T->d_slots + 2 * T->max_chunks,
-                                                              T->d_slots + T->max_chunks, static_cast<int32_t>(n_in),
+                                                              pb, d_slots + 2 * T->max_chunks,
+                                                              d_slots + T->max_chunks, static_cast<int32_t>(n_in),
                                                               kp + l * layer_stride, vp + l * layer_stride);
                 cuda_check(cudaGetLastError(), "swap-in (zero-copy)");
                 count_launch();
@@ -293,7 +328,7 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
                 dst.clear();
                 src.clear();
                 sz.clear();
-                uint8_t* stage_b = T->stage_in + static_cast<int64_t>(l) * n_in * 2 * pb;
+                uint8_t* stage_b = stage_in + static_cast<int64_t>(l) * n_in * 2 * pb;
                 for (int64_t i = 0; i < n_in; ++i) {
                     dst.push_back(stage_b + i * nl * 2 * pb);
                     src.push_back(T->host + static_cast<int64_t>(in_moves[i].src_slot) * T->chunk_bytes() +
@@ -303,7 +338,7 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
                 copy_batch(dst, src, sz, xs);
                 const int grid = static_cast<int>(std::min<int64_t>(n_in * nl * 2, n_sms() * 4));
                 swap_scatter_block_kernel<<<grid, 256, 0, xs>>>(stage_b, kp, vp, layer_stride, l, nl, pb,
-                                                               T->d_slots + T->max_chunks, static_cast<int32_t>(n_in));
+                                                               d_slots + T->max_chunks, static_cast<int32_t>(n_in));
                 cuda_check(cudaGetLastError(), "swap scatter");
                 count_launch();
             }
@@ -316,7 +351,7 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         // 3. swap-out D2H: behind the swap-ins on the copy stream (the reference's order, no
         // duplex contention on the link), or concurrently on its own stream (duplex mode)
         cudaStream_t os = xs;
-        if (T->mode_duplex) {
+        if (T->mode_duplex && !war) {
             os = T->d2h;
             cuda_check(cudaStreamWaitEvent(os, T->gathered, 0), "stream wait");
         }
@@ -326,7 +361,7 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
             sz.clear();
             for (int64_t i = 0; i < n_out; ++i) {
                 dst.push_back(T->host + static_cast<int64_t>(out_moves[i].dst_slot) * T->chunk_bytes());
-                src.push_back(T->stage_out + i * T->chunk_bytes());
+                src.push_back(stage_out + i * T->chunk_bytes());
                 sz.push_back(static_cast<size_t>(T->chunk_bytes()));
             }
             copy_batch(dst, src, sz, os);
@@ -335,10 +370,15 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
                 if (r != PB_OK) fail(r, "swap-out stamp");
             }
         }
-        if (T->mode_duplex) {
+        if (os != xs) {
             cuda_check(cudaEventRecord(T->d2h_done, os), "event record");
             cuda_check(cudaStreamWaitEvent(xs, T->d2h_done, 0), "stream wait");
         }
+        if (n_out > 0) {
+            cuda_check(cudaEventRecord(T->d2h_prev, os), "event record");
+            T->have_prev = true;
+        }
+        cuda_check(cudaEventRecord(T->done_p[par], xs), "event record");
         cuda_check(cudaEventRecord(T->done, xs), "event record");
     });
 }

@@ -93,3 +93,36 @@ def test_cache_moves_drive_the_engine(cuda):
     for c in ids[:5]:
         s = cache.chunk(c).slot
         assert np.array_equal(kn[:, s], truth[c][0]) and np.array_equal(vn[:, s], truth[c][1])
+
+
+def test_host_slot_hazards_across_and_within_steps(cuda):
+    """Host-side hazards of the double-buffered engine: (a) a swap-in in step s+1 from the host
+    slot step s swapped out to (RAW across steps, without a host sync in between) gets the
+    swapped-out bytes; (b) in one step, a swap-in reading host slot X and a swap-out writing X
+    (restore frees X at once, src/paged_kv_cache.cpp:190) -- the swap-in gets the OLD bytes."""
+    torch = cuda
+    L, n_slots, page = 6, 16, 8192
+    k, v = _pools(torch, L, n_slots, page, 4)
+    k0, v0 = k.cpu().numpy().copy(), v.cpu().numpy().copy()
+    tier = KvTier(L, 6, page, 4)
+    host = tier.host_view().reshape(6, L, 2, page)
+    rng = np.random.default_rng(5)
+    host[3] = rng.integers(0, 256, size=(L, 2, page), dtype=np.uint8)
+    old3 = host[3].copy()
+    cs, xs = torch.cuda.Stream(), torch.cuda.Stream()
+    stride = n_slots * page
+    # step 1: device slot 2 -> host slot 0
+    tier.step(k.data_ptr(), v.data_ptr(), stride, [(1, 2, 0)], [], cs.cuda_stream, xs.cuda_stream)
+    # step 2 (issued immediately): host slot 0 -> device slot 9 (RAW on host slot 0), and in the
+    # same step host slot 3 -> device slot 10 while device slot 4 -> host slot 3 (WAR on slot 3)
+    tier.step(k.data_ptr(), v.data_ptr(), stride, [(2, 4, 3)], [(1, 0, 9), (3, 3, 10)], cs.cuda_stream,
+              xs.cuda_stream)
+    for l in range(L):
+        tier.wait_layer(l, cs.cuda_stream)
+    tier.sync()
+    torch.cuda.synchronize()
+    kn, vn = k.cpu().numpy(), v.cpu().numpy()
+    for l in range(L):
+        assert np.array_equal(kn[l, 9], k0[l, 2]) and np.array_equal(vn[l, 9], v0[l, 2])
+        assert np.array_equal(kn[l, 10], old3[l, 0]) and np.array_equal(vn[l, 10], old3[l, 1])
+        assert np.array_equal(host[3, l, 0], k0[l, 4]) and np.array_equal(host[3, l, 1], v0[l, 4])
