@@ -266,7 +266,7 @@ class AttentionPlan:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # lib is None during interpreter shutdown
             lib.pb_attn_plan_destroy(h)
             self._h = None
 
@@ -370,7 +370,7 @@ class KvCache:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # lib is None during interpreter shutdown
             lib.pb_cache_destroy(h)
             self._h = None
 
@@ -523,7 +523,7 @@ class EventLog:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # lib is None during interpreter shutdown
             lib.pb_evlog_destroy(h)
             self._h = None
 
@@ -551,7 +551,7 @@ class KvTier:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
+        if h and lib is not None:  # lib is None during interpreter shutdown
             lib.pb_tier_destroy(h)
             self._h = None
 
