@@ -17,8 +17,8 @@ pytestmark = pytest.mark.gpu
 
 from paper_2312_05516_b200 import abi  # noqa: E402
 from paper_2312_05516_b200.abi import PB_BF16, PB_F32, AttnShape, AttentionPlan, Batch  # noqa: E402
-from paper_2312_05516_b200.workloads import (SplitMix64, Workload, config, random_instance,  # noqa: E402
-                                             unit_draws)
+from paper_2312_05516_b200.workloads import (SplitMix64, Workload, _build, config,  # noqa: E402
+                                             random_instance, unit_draws)
 
 GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
 
@@ -383,3 +383,35 @@ def test_bf16_page_sizes(gh, oracle, chunk):
         assert st == 0
         ok, err = gh.bf16_close(got, want)
         assert ok, (chunk, trial, err, plan.stats())
+
+
+@pytest.mark.parametrize("n_head,n_kv", [(8, 8), (16, 4), (32, 4), (16, 2)])
+def test_fuzz_conversations_with_prefix_drops(gh, oracle, n_head, n_kv):
+    """Random multi-turn shapes as the planner emits them: per conversation a dropped-prefix
+    recompute span (0, a) plus the returning span (b, c) over the same pages, single decode
+    tokens, plain prompts and zero-length spans, all in one ragged batch (one launch)."""
+    for trial in range(6):
+        rng = SplitMix64(7000 + 100 * n_head + 10 * n_kv + trial)
+        convs = []
+        for c in range(1 + rng.next() % 14):
+            kind = rng.next() % 5
+            past = rng.next() % 1800
+            if kind == 0:    # dropped prefix recomputed + the turn's new tokens
+                a = 1 + rng.next() % 300
+                b = a + rng.next() % 400
+                convs.append([(0, a), (b, 1 + rng.next() % 200)])
+            elif kind == 1:  # decode token
+                convs.append([(past, 1)])
+            elif kind == 2:  # prompt over cached history
+                convs.append([(past, 2 + rng.next() % 250)])
+            elif kind == 3:  # zero-length span next to a real one
+                convs.append([(past, 0), (past, 1 + rng.next() % 3)])
+            else:            # fresh prompt
+                convs.append([(0, 1 + rng.next() % 400)])
+        w = _build("fuzz", n_head, n_kv, 128, 16, PB_BF16, rng.seed, convs, rng)
+        q, k, v = gh.device_inputs(w)
+        got, plan = gh.run_plan(w, q, k, v)
+        st, want = oracle.attention(w.shape(), w.batch(), w.host_q(), w.host_pool("k"), w.host_pool("v"))
+        assert st == 0
+        ok, err = gh.bf16_close(got, want)
+        assert ok, (trial, err, plan.stats())
