@@ -55,7 +55,11 @@ struct AttnParams {
     int32_t* counters;       // [n_groups] split arrival counters (self-resetting)
     float* part_ml;          // [n_parts][group][2] running max (log2 domain) and sum
     float* part_o;           // [n_parts][group][head_size] unnormalised outputs
-    int32_t* work_counter;   // persistent-kernel ticket (self-resetting)
+    // workspace counters, all self-resetting (zeroed once per workspace buffer):
+    // [0] SIMT decode next unit, [1] SIMT decode retired warps, [2] fused: next tile item,
+    // [3] fused: retired CTAs, [4] next tcgen05 decode unit, [5] stand-alone decode: retired
+    // CTAs, [6] fused-append grid barrier arrivals, [7] its generation
+    int32_t* work_counter;
     int32_t ablate;          // profiling only (PB_ABLATE): 1 skip softmax math, 2 skip exp
     // fused launch: decode units next to the tile items (items / n_items)
     const WorkItem* dec_items;

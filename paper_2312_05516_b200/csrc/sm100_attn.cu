@@ -72,6 +72,9 @@ constexpr int kLaunchRegs = (65536 / (128 * ((PB_SPLIT ? 4 : 2) + 1))) / 8 * 8;
 static_assert((PB_REG_HI - kLaunchRegs) * (PB_SPLIT ? 4 : 2) <= (kLaunchRegs - PB_REG_LO),
               "setmaxnreg budget exceeds the launch register allocation");
 constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max grows by > 2^8
+#ifndef PB_PV_WAIT_EVERY
+#define PB_PV_WAIT_EVERY 0 // 1: the softmax waits for PV(j-1) on every tile, not only to rescale O
+#endif
 #ifndef PB_MMA_POLL
 #define PB_MMA_POLL 0   // 1: MMA warp issues S(j+1) / PV_A(j) / PV_B(j) in readiness order
 #endif
@@ -90,7 +93,10 @@ struct __align__(1024) Smem {
     uint64_t q_full, q_empty;             // Q is released after the item's last S MMA
     uint64_t k_full[kKvStages], k_empty[kKvStages], v_full[kKvStages], v_empty[kKvStages];
     uint64_t s_full[2][2];                // [query tile][S buffer]
-    uint64_t p_full[2], pv_done[2], o_ready[2], o_empty[2]; // per query tile
+    uint64_t p_full[2][2];                // [query tile][S buffer]: P released (one barrier per
+                                          // buffer, so the softmax can run a tile ahead of the
+                                          // MMA warp without lapping a barrier phase)
+    uint64_t pv_done[2], o_ready[2], o_empty[2]; // per query tile
     uint64_t item_full[kItemRing], item_empty[kItemRing];   // dynamic tile scheduler ring
     uint64_t drain;                       // MMA issuer: every commit of the pass has landed
     int32_t item_ring[kItemRing];
@@ -146,7 +152,8 @@ __device__ __forceinline__ void tile_init(Smem<D>& s) { // thread 0
     for (int i = 0; i < 2; ++i) {
         mbar_init(&s.s_full[i][0], 1);
         mbar_init(&s.s_full[i][1], 1);
-        mbar_init(&s.p_full[i], 128 * kHalves);
+        mbar_init(&s.p_full[i][0], 128 * kHalves);
+        mbar_init(&s.p_full[i][1], 128 * kHalves);
         mbar_init(&s.pv_done[i], 1);
         mbar_init(&s.o_ready[i], 1);
         mbar_init(&s.o_empty[i], 128 * kHalves);
@@ -315,7 +322,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             constexpr uint32_t idesc_o = umma_idesc_bf16(128, D, false, true);
             int it = 0, kst = 0, vst = 0;
             uint32_t kph = 0, vph = 0;
-            uint32_t n_p[2] = {0, 0}, n_oe[2] = {0, 0};
+            uint32_t n_oe[2] = {0, 0};
             uint32_t c_s[2] = {0, 0}, c_p[2] = {0, 0}; // per group: S tiles issued / PV tiles issued
             for (;; ++it) {
                 const int slot = it % kItemRing;
@@ -376,12 +383,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         if (!v_in) v_in = mbar_try_wait(smem_u32(&s.v_full[vst]), vph);
                         if (!v_in) continue;
                         for (int t = 0; t < 2; ++t) {
-                            if (pv[t] || !mbar_try_wait(smem_u32(&s.p_full[t]), n_p[t] & 1)) continue;
+                            if (pv[t] || !mbar_try_wait(smem_u32(&s.p_full[t][c_p[t] & 1]), (c_p[t] >> 1) & 1))
+                                continue;
                             if (j == 0) {
                                 mbar_wait(&s.o_empty[t], (n_oe[t] & 1) ^ 1);
                                 ++n_oe[t];
                             }
-                            ++n_p[t];
                             tc_fence_after();
                             const uint32_t pcol = t * 128 + (c_p[t] & 1) * kBN;
 #pragma unroll
@@ -404,8 +411,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             mbar_wait(&s.o_empty[t], (n_oe[t] & 1) ^ 1);
                             ++n_oe[t];
                         }
-                        mbar_wait(&s.p_full[t], n_p[t] & 1);
-                        ++n_p[t];
+                        mbar_wait(&s.p_full[t][c_p[t] & 1], (c_p[t] >> 1) & 1);
                         tc_fence_after();
                         const uint32_t pcol = t * 128 + (c_p[t] & 1) * kBN; // P (bf16) over S
 #pragma unroll
@@ -486,9 +492,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                 mbar_wait(&s.s_full[t][b], (c_t >> 1) & 1);
                 tc_fence_after();
                 if (p.ablate == 1) { // profiling: tensor-core + pipeline bound (P left as S bits)
-                    if (c_t > 0) mbar_wait(&s.pv_done[t], (c_t - 1) & 1);
                     tc_fence_before();
-                    mbar_arrive(&s.p_full[t]);
+                    mbar_arrive(&s.p_full[t][b]);
                     l_run = 1.f;
                     continue;
                 }
@@ -560,11 +565,13 @@ __global__ void __launch_bounds__(kThreads, 1)
                     if constexpr (kCols == 64) tmem_st32(t_lane + col_s, *reinterpret_cast<uint32_t(*)[32]>(pk));
                     else dtc::tmem_st16(t_lane + col_s + hf * (kCols / 2), *reinterpret_cast<uint32_t(*)[16]>(pk));
                 }
-                // PV_t of the previous tile must be complete before O_t is rescaled and before
-                // P_t(j) is released; waiting on it every tile also keeps pv_done at most one
-                // phase behind, so its parity wait is exact
-                if (c_t > 0) mbar_wait(&s.pv_done[t], (c_t - 1) & 1);
-                if (j > 0 && __any_sync(0xffffffffu, grow)) {
+                // O_t may only be rescaled once PV_t of the previous tile is complete.  The
+                // parity wait is exact without waiting every tile: S_t(j) landed, and it was
+                // issued after PV_t(j-2) on the in-order tensor pipe, so pv_done is at most
+                // one phase behind (PV_t(j) cannot start before this thread releases P_t(j)).
+                const bool rescale = j > 0 && __any_sync(0xffffffffu, grow);
+                if (PB_PV_WAIT_EVERY ? c_t > 0 : rescale) mbar_wait(&s.pv_done[t], (c_t - 1) & 1);
+                if (rescale) {
                     tc_fence_after();
 #pragma unroll
                     for (int c = 0; c < kOCols / 32; ++c) {
@@ -578,7 +585,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
                 tmem_st_wait();
                 tc_fence_before();
-                mbar_arrive(&s.p_full[t]);
+                mbar_arrive(&s.p_full[t][b]);
                 const float2 s2 = add2(add2(ps[0], ps[1]), add2(ps[2], ps[3]));
                 const float sum = s2.x + s2.y;
                 l_run = l_run * corr + sum;

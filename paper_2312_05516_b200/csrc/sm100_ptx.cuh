@@ -49,12 +49,15 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
     // debugging builds only: a wait that lasts ~2 s reports the barrier and traps, so a
     // pipeline bug ends the launch with an error instead of hanging the GPU
     const long long t0 = clock64();
+    bool said = false;
     while (!mbar_try_wait(a, parity)) {
-        if (clock64() - t0 > 4000000000LL) {
+        const long long dt = clock64() - t0;
+        if (!said && dt > 4000000000LL) {
             printf("PB_WATCHDOG: block %d thread %d stuck on smem barrier 0x%x parity %u\n", blockIdx.x,
                    threadIdx.x, a, parity);
-            __trap();
+            said = true;
         }
+        if (dt > 12000000000LL) __trap();
     }
 #else
     while (!mbar_try_wait(a, parity)) {

@@ -19,9 +19,13 @@ from paper_2312_05516_b200.abi import AttentionPlan  # noqa: E402
 from paper_2312_05516_b200.workloads import config  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 2
+world = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # rank 0 of an N-way kv-head shard
 w = config(cfg)
+from paper_2312_05516_b200.sharding import shard_shape  # noqa: E402
+shape = shard_shape(w.shape(), 0, world)
+w.n_kv_head, w.n_head = shape.n_kv_head, shape.n_head
 q, k, v = gh.device_inputs(w)
-plan = AttentionPlan(w.shape(), w.batch())
+plan = AttentionPlan(shape, w.batch())
 stream = torch.cuda.current_stream().cuda_stream
 plan.upload(stream)
 out = torch.empty_like(q)
@@ -40,7 +44,7 @@ for b in range(148):
         mode, _, beg, end = t[b, ps]
         if beg > 0:
             rows.append((b, ps, int(mode), (beg - t0) / 1e3, (end - t0) / 1e3))
-res = {"config": cfg, "stats": plan.stats()}
+res = {"config": cfg, "world": world, "stats": plan.stats()}
 for mode in (0, 1):
     first = [r for r in rows if r[1] == 0 and r[2] == mode]
     second = [r for r in rows if r[1] == 1 and r[2] == mode]
