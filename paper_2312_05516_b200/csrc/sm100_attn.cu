@@ -75,9 +75,6 @@ constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max gr
 #ifndef PB_PV_WAIT_EVERY
 #define PB_PV_WAIT_EVERY 0 // 1: the softmax waits for PV(j-1) on every tile, not only to rescale O
 #endif
-#ifndef PB_S_PREFETCH
-#define PB_S_PREFETCH 0 // 1: the softmax reads S(j+1) from TMEM while it processes tile j
-#endif
 #ifndef PB_MMA_POLL
 #define PB_MMA_POLL 0   // 1: MMA warp issues S(j+1) / PV_A(j) / PV_B(j) in readiness order
 #endif
@@ -129,25 +126,6 @@ __device__ __forceinline__ ItemTiles item_tiles(const WorkItem& w, const SpanDev
     r.ntiles[1] = r.nt[1] > 0 ? ceil_div(sp.causal_offset + w.t0 + w.nt, kBN) : 0;
     r.n_kv = max(r.ntiles[0], r.ntiles[1]);
     return r;
-}
-
-// tcgen05.wait::ld that also "redefines" r, so no use of r is scheduled above the wait
-template <int N>
-__device__ __forceinline__ void tmem_ld_wait_regs(float (&r)[N]) {
-    static_assert(N % 32 == 0, "groups of 32 registers");
-    tmem_ld_wait();
-#pragma unroll
-    for (int i = 0; i < N; i += 32) {
-        uint32_t* u = reinterpret_cast<uint32_t*>(&r[i]);
-        asm volatile(""
-                     : "+r"(u[0]), "+r"(u[1]), "+r"(u[2]), "+r"(u[3]), "+r"(u[4]), "+r"(u[5]), "+r"(u[6]),
-                       "+r"(u[7]), "+r"(u[8]), "+r"(u[9]), "+r"(u[10]), "+r"(u[11]), "+r"(u[12]), "+r"(u[13]),
-                       "+r"(u[14]), "+r"(u[15]), "+r"(u[16]), "+r"(u[17]), "+r"(u[18]), "+r"(u[19]),
-                       "+r"(u[20]), "+r"(u[21]), "+r"(u[22]), "+r"(u[23]), "+r"(u[24]), "+r"(u[25]),
-                       "+r"(u[26]), "+r"(u[27]), "+r"(u[28]), "+r"(u[29]), "+r"(u[30]), "+r"(u[31])
-                     :
-                     : "memory");
-    }
 }
 
 // A operand in TMEM (P, bf16), B from shared memory (V).
@@ -508,21 +486,10 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int tok0 = w.t0 + t * tpt;           // first span-relative token of this tile
             const int allowed = sp.causal_offset + tok0 + (valid ? t_local : 0) + 1;
             float m_run = -CUDART_INF_F, l_run = 0.f;
-#if PB_S_PREFETCH
-            float xn[kCols];      // S of the next tile, read from TMEM while this one is processed
-            bool have_next = false;
-#endif
             for (int j = 0; j < n_tiles; ++j, ++c_t) {
                 const uint32_t b = c_t & 1;
                 const uint32_t col_s = t * 128 + b * kBN;
                 float x[kCols];
-#if PB_S_PREFETCH
-                if (have_next) {
-                    tmem_ld_wait_regs<kCols>(xn);
-#pragma unroll
-                    for (int c = 0; c < kCols; ++c) x[c] = xn[c];
-                } else
-#endif
                 {
                     mbar_wait(&s.s_full[t][b], (c_t >> 1) & 1);
                     tc_fence_after();
@@ -537,19 +504,6 @@ __global__ void __launch_bounds__(kThreads, 1)
                         tmem_ld32(t_lane + col_s + hf * kCols + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
                     tmem_ld_wait();
                 }
-#if PB_S_PREFETCH
-                // start reading the next tile's S now if it has landed (no wait otherwise)
-                have_next = false;
-                if (j + 1 < n_tiles &&
-                    mbar_try_wait(smem_u32(&s.s_full[t][(c_t + 1) & 1]), ((c_t + 1) >> 1) & 1)) {
-                    tc_fence_after();
-                    const uint32_t col_n = t * 128 + ((c_t + 1) & 1) * kBN;
-#pragma unroll
-                    for (int c = 0; c < kCols / 32; ++c)
-                        tmem_ld32(t_lane + col_n + hf * kCols + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&xn[c * 32]));
-                    have_next = true;
-                }
-#endif
                 const int kv0 = j * kBN + hf * kCols;
                 const bool diag = kv0 + kCols > allowed;
                 float pm[8];
