@@ -94,7 +94,10 @@ pb_status pb_attn_plan_create(const pb_attn_shape* shape, int32_t n_spans,
                               int64_t total_tokens, int32_t flags, pb_attn_plan** out);
 /* Copies the plan's descriptors to the device on `stream` (first call allocates). */
 pb_status pb_attn_plan_upload(pb_attn_plan* plan, void* stream);
-/* Device workspace bytes pb_attn_run needs (split-KV partials + tile counters). */
+/* Device workspace bytes pb_attn_run needs (split-KV partials + work-queue counters).  The
+ * counters are zeroed on first use of a workspace buffer and are self-resetting after
+ * every launch, so one workspace serves a whole layer loop; it must not be shared by two
+ * launches that can run at the same time (give each stream its own). */
 size_t pb_attn_plan_workspace_bytes(const pb_attn_plan* plan);
 /* Plan statistics: out[0] prefill tiles, [1] decode units, [2] split spans,
  * [3] algorithmic flops (4*n_head*d*sum allowed), [4] algorithmic bytes, [5] total tokens,
