@@ -1,26 +1,28 @@
-// sm_100a tile path of the fused ragged paged attention: multi-token spans (prefill, prompt
-// and dropped-prefix recompute spans) on the 5th-generation tensor cores.
+// The fused ragged paged attention launch for sm_100a: multi-token spans (prefill, prompt
+// and dropped-prefix recompute spans) as tcgen05 tiles, single-token spans as tcgen05
+// split-KV units (decode_tc_cta.cuh), from two persistent queues in one kernel.
 //
 // Semantics: paged_multi_token_attention, /root/reference/proj/src/attention.cpp:73-132
 // (token i of a span sees [0, causal_offset+i], head h reads kv head h/group, softmax with
-// max subtraction).  B200 design:
+// max subtraction).  Tile pipeline:
 //   * one work item = (span, kv head, block of 2 x 128/group query tokens) = two M=128 query
 //     tiles A and B that share every K/V tile loaded; the GQA group is packed into M
-//     (rows = tokens x heads-of-the-group), PAPER.md:708-717 fuses QK^T, mask, softmax, PV;
+//     (rows = tokens x heads-of-the-group); PAPER.md:708-717 fuses QK^T, mask, softmax, PV;
 //   * persistent CTAs, 3 warpgroups: WG0 / WG1 = softmax + correction + epilogue of query
-//     tiles A / B (one TMEM lane = one query row per thread, 224 registers via setmaxnreg),
+//     tiles A / B (one TMEM lane = one query row per thread, 208 registers via setmaxnreg),
 //     WG2 = warp 8 TMA producer + warp 9 MMA issuer (one elected thread,
-//     tcgen05.mma.cta_group::1.kind::f16) at 56 registers;
-//   * TMEM: S_A | S_B | O_A | O_B (4 x 128 columns).  P (bf16) is written back over S with
-//     tcgen05.st and fed to the PV MMA straight from TMEM (A operand in TMEM), so P never
-//     touches shared memory;
-//   * MMA order per KV tile j: PV_A(j), S_A(j+1), PV_B(j), S_B(j+1): while one softmax group
-//     works on its scores the tensor core runs the other group's two MMAs (ping-pong);
-//   * KV pages are gathered straight from the paged pools by TMA: a 128-row KV tile is
-//     128/page_tokens box loads {64 dims, 1 kv head, page_tokens rows} at row coordinate
+//     tcgen05.mma.cta_group::1.kind::f16) at 88 registers;
+//   * kv tiles of 64 rows; TMEM: S_A[2] | S_B[2] (64 columns each, double-buffered so S(j+1)
+//     is computed while the softmax turns S(j) into P(j)) | O_A | O_B (128 each).  P (bf16)
+//     is written back over its S buffer with tcgen05.st and fed to the PV MMA from TMEM;
+//   * MMA issue per kv tile j: S_A(j+1), S_B(j+1), then PV_A(j) and PV_B(j) as each group
+//     releases P; one p_full barrier per S buffer lets a group run a tile ahead;
+//   * KV pages are gathered straight from the paged pools by TMA: a 64-row kv tile is
+//     64/page_tokens box loads {64 dims, 1 kv head, page_tokens rows} per 64-dim half at row
 //     block_table[p] * page_tokens (SWIZZLE_128B); pages past the span's table are fetched
 //     out of bounds, which TMA zero-fills;
 //   * O is rescaled lazily (only when a row's running max grows by more than 2^8).
+// DESIGN.md §3 has the measurements behind each choice and the pipeline invariants.
 #include "attn_internal.hpp"
 #include "pb_common.hpp"
 #include "sm100_attn.hpp"
