@@ -126,8 +126,6 @@ def select_cpu_sample(w, threads: int, budget_s: float):
 def run_reference_cpu(w, threads: int, budget_s: float, reps: int = 1):
     """The reference's own paged_multi_token_attention (oracle/_ref), per sub-request on
     `threads` host threads, over a bounded span sample.  Returns (seconds, flops, bytes, ids)."""
-    import numpy as np
-
     from oracle.oracle import Reference
 
     ids = select_cpu_sample(w, threads, budget_s)

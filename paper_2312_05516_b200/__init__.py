@@ -6,9 +6,6 @@ never computes anything itself and fails loudly when the native library is missi
 """
 from __future__ import annotations
 
-import ctypes
-import os
-
 from . import abi
 from .abi import (  # noqa: F401
     PB_BF16,

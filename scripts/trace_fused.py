@@ -11,7 +11,6 @@ ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 
-import numpy as np  # noqa: E402
 import torch  # noqa: E402
 
 import gpu_helpers as gh  # noqa: E402

@@ -7,7 +7,6 @@ bf16-rounded inputs widened to fp32.  Full-size configs are checked on sampled s
 spans are independent units) plus size-independent properties.
 """
 import json
-import math
 import os
 
 import numpy as np
