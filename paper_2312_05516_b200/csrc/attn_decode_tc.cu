@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(kDtThreads, 1)
     tc_fence_after();
     const uint32_t tmem = s.tmem_base;
     int* ctr = p.work_counter; // [4] next unit, [5] retired CTAs (self-resetting)
-    decode_cta_run<G>(s, tmem, &tm_q, &tm_k, &tm_v, p, p.items, p.n_items, ctr + 4, 0, 1, 2);
+    decode_cta_run<G>(s, tmem, &tm_q, &tm_k, &tm_v, p, p.items, p.n_items, ctr + 4, 0, 1, 2, 6);
     tc_fence_before();
     __syncthreads();
     if (threadIdx.x == 0) {

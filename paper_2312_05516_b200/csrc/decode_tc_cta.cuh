@@ -37,7 +37,7 @@ namespace dtc {
 
 using namespace pb::sm100;
 
-constexpr int kDtThreads = 192;
+constexpr int kDtThreads = 224;     // TMA K warp, MMA warp, 4 softmax warps, TMA V warp
 constexpr int kKvRows = 128;         // kv rows per tile
 constexpr int kN = 16;               // padded query heads (N of both MMAs)
 constexpr int kStages = 3;           // K/V ring depth
@@ -46,7 +46,7 @@ constexpr uint32_t kTmemCols = 64;   // S^T buffers [0,16) [16,32), O^T [32,48)
 constexpr uint32_t kColO = 32;
 constexpr float kThr = 8.f;          // lazy rescale threshold (log2 domain)
 constexpr uint32_t kHalf = kKvRows * 128;          // one 64-dim half of a kv tile (16 KB)
-constexpr uint32_t kStageTx = 2u * 2u * kHalf;     // K + V, two halves each (D = 128)
+constexpr uint32_t kStageTx = 2u * kHalf;          // one of K or V, two halves (D = 128)
 
 struct __align__(1024) DtSmem {
     uint8_t k[kStages][2][kHalf];   // [stage][half][row][128 B], SW128 K-major (A of S^T)
@@ -56,7 +56,9 @@ struct __align__(1024) DtSmem {
     float red[2][4][kN];            // [tile parity][warp quadrant][head] max exchange
     float redl[4][kN];              // [warp quadrant][head] epilogue sum exchange
     int32_t flag;
-    uint64_t kv_full[kStages], kv_empty[kStages];
+    // separate K and V rings with their own producer warps: a K stage is free as soon as S
+    // has read it, so K runs further ahead and more bytes are in flight per CTA
+    uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
     uint64_t q_full[2], q_empty[2];
     uint64_t s_full[2], p_full, pv_done, o_empty;
     uint64_t item_full[kRing], item_empty[kRing];
@@ -98,8 +100,10 @@ __device__ __forceinline__ int unit_tiles(const WorkItem& w, int chunk) {
 // thread 0 only: the decode pipeline's barriers
 __device__ __forceinline__ void decode_cta_init(DtSmem& s) {
     for (int i = 0; i < kStages; ++i) {
-        mbar_init(&s.kv_full[i], 1);
-        mbar_init(&s.kv_empty[i], 1);
+        mbar_init(&s.k_full[i], 1);
+        mbar_init(&s.k_empty[i], 1);
+        mbar_init(&s.v_full[i], 1);
+        mbar_init(&s.v_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
         mbar_init(&s.q_full[i], 1);
@@ -111,7 +115,7 @@ __device__ __forceinline__ void decode_cta_init(DtSmem& s) {
     mbar_init(&s.o_empty, 128);
     for (int i = 0; i < kRing; ++i) {
         mbar_init(&s.item_full[i], 1);
-        mbar_init(&s.item_empty[i], 1 + 4); // MMA thread + 4 softmax warps
+        mbar_init(&s.item_empty[i], 1 + 4 + 1); // MMA thread + 4 softmax warps + V producer
     }
     mbar_init(&s.drain, 1);
 }
@@ -119,8 +123,10 @@ __device__ __forceinline__ void decode_cta_init(DtSmem& s) {
 // thread 0 only, pipeline drained: release the barriers' memory for another layout
 __device__ __forceinline__ void decode_cta_inval(DtSmem& s) {
     for (int i = 0; i < kStages; ++i) {
-        mbar_inval(&s.kv_full[i]);
-        mbar_inval(&s.kv_empty[i]);
+        mbar_inval(&s.k_full[i]);
+        mbar_inval(&s.k_empty[i]);
+        mbar_inval(&s.v_full[i]);
+        mbar_inval(&s.v_empty[i]);
     }
     for (int i = 0; i < 2; ++i) {
         mbar_inval(&s.q_full[i]);
@@ -137,15 +143,15 @@ __device__ __forceinline__ void decode_cta_inval(DtSmem& s) {
     mbar_inval(&s.drain);
 }
 
-// One CTA of the decode pipeline.  Roles: warp w_prod = TMA producer, w_mma = MMA issuer,
-// w_sm0 .. w_sm0+3 = softmax + epilogue (must cover the four TMEM lane quadrants); other warps
-// fall through.  Units come from `items` through the global `ticket`.  TMEM columns
+// One CTA of the decode pipeline.  Roles: warp w_prod = TMA producer of q and K (and the
+// unit ticket), w_prodv = TMA producer of V, w_mma = MMA issuer, w_sm0 .. w_sm0+3 = softmax +
+// epilogue (must cover the four TMEM lane quadrants); other warps fall through.  Units come from `items` through the global `ticket`.  TMEM columns
 // [tmem, tmem + 48) are used.
 template <int G>
 __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, const CUtensorMap* tm_q,
                                                const CUtensorMap* tm_k, const CUtensorMap* tm_v, const AttnParams& p,
                                                const WorkItem* items, const int n_items, int* ticket, const int w_prod,
-                                               const int w_mma, const int w_sm0) {
+                                               const int w_mma, const int w_sm0, const int w_prodv) {
     constexpr int D = 128;
     const int warp = threadIdx.x >> 5;
     const int lane = threadIdx.x & 31;
@@ -185,16 +191,49 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                         const int page = j * ppt + pg;
                         rows[pg] = (pg < ppt && page < np) ? __ldg(table + page) * chunk : oob_row;
                     }
-                    mbar_wait(&s.kv_empty[stage], kph ^ 1);
-                    mbar_arrive_expect_tx(&s.kv_full[stage], kStageTx);
+                    mbar_wait(&s.k_empty[stage], kph ^ 1);
+                    mbar_arrive_expect_tx(&s.k_full[stage], kStageTx);
 #pragma unroll
                     for (int pg = 0; pg < 16; ++pg)
                         if (pg < ppt)
-                            for (int h = 0; h < 2; ++h) {
-                                tma_load_3d(s.k[stage][h] + pg * chunk * 128, tm_k, &s.kv_full[stage], h * 64, w.kvh, rows[pg]);
-                                tma_load_3d(s.v[stage][h] + pg * chunk * 128, tm_v, &s.kv_full[stage], h * 64, w.kvh, rows[pg]);
-                            }
+                            for (int h = 0; h < 2; ++h)
+                                tma_load_3d(s.k[stage][h] + pg * chunk * 128, tm_k, &s.k_full[stage], h * 64, w.kvh, rows[pg]);
                     if (++stage == kStages) { stage = 0; kph ^= 1; }
+                }
+            }
+        }
+    } else if (warp == w_prodv) {
+        // ============================ TMA producer (V) ========================
+        if (elect_one()) {
+            int stage = 0;
+            uint32_t vph = 0;
+            const int oob_row = p.n_slots * chunk;
+            for (int it = 0;; ++it) {
+                const int slot = it % kRing;
+                mbar_wait(&s.item_full[slot], (it / kRing) & 1);
+                const int item = *reinterpret_cast<volatile int32_t*>(&s.item_ring[slot]);
+                mbar_arrive(&s.item_empty[slot]);
+                if (item < 0) break;
+                const WorkItem w = items[item];
+                const SpanDev sp = p.spans[w.span];
+                const int32_t* table = p.block_tables + sp.bt_off + w.kv_begin / chunk;
+                const int np = (w.kv_end - w.kv_begin + chunk - 1) / chunk;
+                const int nt = (np + ppt - 1) / ppt;
+                for (int j = 0; j < nt; ++j) {
+                    int rows[16];
+#pragma unroll
+                    for (int pg = 0; pg < 16; ++pg) {
+                        const int page = j * ppt + pg;
+                        rows[pg] = (pg < ppt && page < np) ? __ldg(table + page) * chunk : oob_row;
+                    }
+                    mbar_wait(&s.v_empty[stage], vph ^ 1);
+                    mbar_arrive_expect_tx(&s.v_full[stage], kStageTx);
+#pragma unroll
+                    for (int pg = 0; pg < 16; ++pg)
+                        if (pg < ppt)
+                            for (int h = 0; h < 2; ++h)
+                                tma_load_3d(s.v[stage][h] + pg * chunk * 128, tm_v, &s.v_full[stage], h * 64, w.kvh, rows[pg]);
+                    if (++stage == kStages) { stage = 0; vph ^= 1; }
                 }
             }
         }
@@ -203,8 +242,10 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
         if (elect_one()) {
             constexpr uint32_t idesc_s = umma_idesc_bf16(128, kN, false, false);
             constexpr uint32_t idesc_o = umma_idesc_bf16(128, kN, true, false);
-            int stage = 0;
+            int stage = 0;   // K ring position (the tile S is issued for)
             uint32_t kph = 0;
+            int vstage = 0;  // V ring position (the tile PV is issued for)
+            uint32_t vph = 0;
             uint32_t T = 0; // tiles issued by this CTA (all units)
             auto issue_s = [&](int qb, uint32_t tile) {
                 const uint64_t ad = umma_desc_sw128(smem_u32(s.k[stage][0]), 16, 1024);
@@ -216,6 +257,8 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                     umma_bf16_ss(tmem + (tile & 1) * kN, ad + oa, bd + ob, idesc_s, kk > 0);
                 }
                 umma_commit(&s.s_full[tile & 1]);
+                umma_commit(&s.k_empty[stage]); // K is read by S only
+                if (++stage == kStages) { stage = 0; kph ^= 1; }
             };
             for (int it = 0;; ++it) {
                 const int slot = it % kRing;
@@ -231,21 +274,20 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                 const int nt = unit_tiles(w, chunk);
                 const int qb = it & 1;
                 mbar_wait(&s.q_full[qb], (it >> 1) & 1);
-                mbar_wait(&s.kv_full[stage], kph);
+                mbar_wait(&s.k_full[stage], kph);
                 tc_fence_after();
                 issue_s(qb, T);
                 for (int j = 0; j < nt; ++j, ++T) {
-                    const int cur = stage;
-                    if (++stage == kStages) { stage = 0; kph ^= 1; }
                     if (j + 1 < nt) { // S(j+1) overlaps softmax(j)
-                        mbar_wait(&s.kv_full[stage], kph);
+                        mbar_wait(&s.k_full[stage], kph);
                         tc_fence_after();
                         issue_s(qb, T + 1);
                     }
                     mbar_wait(&s.p_full, T & 1);
                     if (j == 0 && it > 0) mbar_wait(&s.o_empty, (it - 1) & 1);
+                    mbar_wait(&s.v_full[vstage], vph);
                     tc_fence_after();
-                    const uint64_t ad = umma_desc_sw128(smem_u32(s.v[cur][0]), kHalf, 1024);
+                    const uint64_t ad = umma_desc_sw128(smem_u32(s.v[vstage][0]), kHalf, 1024);
                     const uint64_t bd = umma_desc_sw128(smem_u32(s.pt[T & 1][0]), 16, 1024);
 #pragma unroll
                     for (int kk = 0; kk < kKvRows / 16; ++kk) {
@@ -253,7 +295,8 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                         umma_bf16_ss(tmem + kColO, ad + kk * (2048 >> 4), bd + ob, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
                     }
                     umma_commit(&s.pv_done);
-                    umma_commit(&s.kv_empty[cur]);
+                    umma_commit(&s.v_empty[vstage]);
+                    if (++vstage == kStages) { vstage = 0; vph ^= 1; }
                 }
                 umma_commit(&s.q_empty[qb]);
             }
@@ -335,6 +378,9 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                     // rows past the unit's end in a fetched page may hold anything (stale or
                     // never-written pool rows): zero their V so 0 * NaN cannot reach O
                     const int stg = static_cast<int>(T % kStages);
+                    // V arrives on its own ring: wait until this tile's V landed before zeroing
+                    // (its next reuse needs PV(T), so the parity wait is exact)
+                    mbar_wait(&s.v_full[stg], (T / kStages) & 1);
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
 #pragma unroll

@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (dec) {
         if constexpr (D == 128)
             dtc::decode_cta_run<GD>(ds, tmem, &tm_qd, &tm_k, &tm_v, p, p.dec_items, p.n_dec_items, ctr + 4, kProdWarp,
-                                    kMmaWarp, 0);
+                                    kMmaWarp, 0, kProdWarp + 2);
     } else if (warp == kProdWarp) {
         // ============================ TMA producer ============================
         if (elect_one()) {
@@ -442,7 +442,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (dec) {
         if constexpr (D == 128)
             dtc::decode_cta_run<GD>(ds, tmem, &tm_qd, &tm_k, &tm_v, p, p.dec_items, p.n_dec_items, ctr + 4, kProdWarp,
-                                    kMmaWarp, 0);
+                                    kMmaWarp, 0, kProdWarp + 2);
     } else {
         // ============ softmax / correction / epilogue (one group per query tile) ============
         // kHalves softmax warpgroups per query tile: warpgroup wg serves tile wg & 1 and the
