@@ -514,6 +514,9 @@ def bench_config5(args):
     torch.cuda.synchronize()
     events = log.read()
     tier.set_event_log(None)
+    if os.environ.get("PB_CFG5_DUMP"):  # diagnostics: the device-stamped per-layer timeline
+        import numpy as np
+        np.save(os.environ["PB_CFG5_DUMP"], events)
     violations, audited_steps = abi.audit_events(events, per_step=True)
     timed = steps[args.warmup:args.warmup + args.steps]
     attn_bytes = sum(pl.stats()["bytes"] for pl in plans[args.warmup:args.warmup + args.steps]) * n_layer

@@ -133,7 +133,11 @@ void build_work(pb_attn_plan& P) {
                     sm100_supports(s.head_size, s.chunk_size, g);
     // SIMT tiles: blocks of tokens, ~16 rows per warp-pass
     const int simt_tokens = std::max(1, 32 / g);
-    const int tc_tokens = tc ? sm100_tile_tokens(g) : 0;
+    static const int tile_half = [] { // profiling: one query tile per item instead of two
+        const char* e = std::getenv("PB_TILE_HALF");
+        return e ? std::atoi(e) : 0;
+    }();
+    const int tc_tokens = tc ? sm100_tile_tokens(g) / (tile_half ? 2 : 1) : 0;
     P.decode_kernel = tc && (decode_supports(s.head_size, s.chunk_size, g) ||
                              decode_tc_supports(s.head_size, s.chunk_size, g));
     std::vector<std::pair<double, WorkItem>> tc_list, dec_list;
@@ -192,7 +196,7 @@ void build_work(pb_attn_plan& P) {
                     const double kv = sp.causal_offset + w.t0 + w.nt;
                     // est. SM cycles: a 128-position kv tile is ~3400 cycles for two
                     // query tiles at the measured MMA/softmax rate
-                    tc_list.push_back({kv * (w.nt > tc_tokens / 2 ? 26.5 : 13.3), w});
+                    tc_list.push_back({kv * (w.nt > sm100_tile_tokens(g) / 2 ? 26.5 : 13.3), w});
                     ++P.n_prefill;
                 }
             } else if (!P.decode_kernel) {
@@ -504,10 +508,15 @@ static void run_impl(pb_attn_plan* P, const void* q, const void* k_pages, const 
         // pb_attn_run's stream continues.
         if (P->fused && only == 0) {
             // one launch: tile items and decode units from two queues (sm100_attn.cu)
-            static const double cta_scale = [] {
+            static const double cta_scale_env = [] {
                 const char* e = std::getenv("PB_DEC_CTA_SCALE"); // profiling knob
-                return e ? std::atof(e) : 1.0;
+                return e ? std::atof(e) : 0.0;
             }();
+            // A decode CTA next to tensor-bound tiles streams slower than 1/148 of HBM, so a
+            // small decode share is under-estimated: double it below 25% (measured: cfg4 at an
+            // 8-way kv-head shard 92 -> 83 us per layer, unchanged at N = 1; cfg2, where decode
+            // is most of the launch, is best unscaled, profiles/r1_variants.md).
+            const double cta_scale = cta_scale_env > 0 ? cta_scale_env : (P->dec_share < 0.25 ? 2.0 : 1.0);
             AttnParams pf = p;
             pf.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_tc);
             pf.n_items = static_cast<int32_t>(P->tc_items.size());

@@ -12,7 +12,10 @@
 //   * the swap-out GATHER (device pages -> contiguous staging) runs first, on the compute
 //     stream, so device slots vacated by swap-out can be refilled in the same step by restore /
 //     rematerialize / append (the reference reuses them LIFO, src/paged_kv_cache.cpp:28-37)
-//     without a read-after-write hazard; the swap-in scatter waits for that gather.
+//     without a read-after-write hazard; the swap-in scatter waits for that gather;
+//   * across steps the D2H is decoupled from the copy stream: a step's swap-ins wait for the
+//     previous step's D2H only when they read a host slot it writes, and a D2H waits for the
+//     previous step's swap-ins (a host slot freed by restore may be reused at once).
 // Host tier layout: [host_slot][layer][K|V][page] — one chunk's bytes for all layers are
 // contiguous (= ModelConfig::chunk_bytes per worker, src/model_config.cpp:36-40), so a
 // swap-out is one D2H per chunk; a swap-in reads one (K,V) block per chunk per layer.
@@ -154,13 +157,13 @@ struct pb_kv_tier {
     uint8_t* stage_in[2] = {};     // device [layer block][chunk][layers][K|V][page]
     int32_t* d_slots[2] = {};      // device: [out src slots | in dst slots | in host src slots]
     int32_t* h_slots[2] = {};      // pinned staging for the slot lists
-    cudaEvent_t done_p[2] = {};    // step with this parity fully done (transfers + D2H)
+    cudaEvent_t done_p[2] = {};    // swap-ins of the step with this parity done (copy stream)
+    cudaEvent_t d2h_p[2] = {};     // swap-out D2H of the step with this parity done
     cudaEvent_t d2h_prev = nullptr; // last issued swap-out D2H (host-slot RAW for swap-ins)
+    std::vector<int32_t> prev_out_dst; // host slots the previous step's D2H writes (sorted)
     int par = 0;
-    bool have_prev = false;
     const uint8_t* host_dev = nullptr; // device alias of the pinned tier (zero-copy swap-in)
     cudaStream_t d2h = nullptr;    // duplex mode: swap-out D2H on its own stream
-    cudaEvent_t d2h_done = nullptr;
     int mode_zc = 0, mode_duplex = 0;
     int layer_block = 1;           // staged swap-in: layers per H2D piece (larger pieces, coarser events)
     pb_event_log* log = nullptr;   // optional: stamps SWAP_IN_LAYER / SWAP_OUT
@@ -201,6 +204,7 @@ pb_status pb_tier_create(int32_t n_layer, int32_t host_slots, int64_t page_bytes
                                      cudaHostAllocPortable),
                        "cudaHostAlloc(slots)");
             cuda_check(cudaEventCreateWithFlags(&T->done_p[b], cudaEventDisableTiming), "event");
+            cuda_check(cudaEventCreateWithFlags(&T->d2h_p[b], cudaEventDisableTiming), "event");
         }
         cuda_check(cudaEventCreateWithFlags(&T->d2h_prev, cudaEventDisableTiming), "event");
         void* hd = nullptr;
@@ -215,7 +219,6 @@ pb_status pb_tier_create(int32_t n_layer, int32_t host_slots, int64_t page_bytes
         const char* lb = std::getenv("PB_SWAP_LB");
         T->layer_block = std::max(1, std::min(n_layer, lb ? std::atoi(lb) : kDefaultLayerBlock));
         cuda_check(cudaStreamCreateWithFlags(&T->d2h, cudaStreamNonBlocking), "d2h stream");
-        cuda_check(cudaEventCreateWithFlags(&T->d2h_done, cudaEventDisableTiming), "event");
         cuda_check(cudaEventCreateWithFlags(&T->gathered, cudaEventDisableTiming), "event");
         cuda_check(cudaEventCreateWithFlags(&T->done, cudaEventDisableTiming), "event");
         T->layer_ready.resize(static_cast<size_t>(n_layer));
@@ -232,6 +235,10 @@ void pb_tier_destroy(pb_kv_tier* T) {
             cudaEventSynchronize(T->done_p[b]);
             cudaEventDestroy(T->done_p[b]);
         }
+        if (T->d2h_p[b]) {
+            cudaEventSynchronize(T->d2h_p[b]);
+            cudaEventDestroy(T->d2h_p[b]);
+        }
         cudaFree(T->stage_out[b]);
         cudaFree(T->stage_in[b]);
         cudaFree(T->d_slots[b]);
@@ -243,7 +250,6 @@ void pb_tier_destroy(pb_kv_tier* T) {
         cudaStreamSynchronize(T->d2h);
         cudaStreamDestroy(T->d2h);
     }
-    if (T->d2h_done) cudaEventDestroy(T->d2h_done);
     if (T->gathered) cudaEventDestroy(T->gathered);
     if (T->done) cudaEventDestroy(T->done);
     for (auto e : T->layer_ready) cudaEventDestroy(e);
@@ -272,6 +278,7 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         const int par = T->par;
         T->par ^= 1;
         cuda_check(cudaEventSynchronize(T->done_p[par]), "swap step ordering");
+        cuda_check(cudaEventSynchronize(T->d2h_p[par]), "swap step ordering");
         int32_t* h_slots = T->h_slots[par];
         int32_t* d_slots = T->d_slots[par];
         uint8_t* stage_out = T->stage_out[par];
@@ -281,10 +288,14 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         for (int64_t i = 0; i < n_in; ++i) h_slots[2 * T->max_chunks + i] = in_moves[i].src_slot;
         cuda_check(cudaMemcpyAsync(d_slots, h_slots, sizeof(int32_t) * 3 * T->max_chunks, cudaMemcpyHostToDevice, cs),
                    "slot upload");
-        // host-slot hazards: a swap-in may read a host slot the previous step's swap-out wrote
-        // (RAW: the swap-ins wait for that D2H), and restore frees host slots at once, so this
-        // step's swap-out may overwrite a slot one of this step's swap-ins reads (WAR: then the
-        // D2H waits for the swap-ins, the reference's order, src/swap_engine.cpp:50-53)
+        // host-slot hazards: a swap-in may read a host slot the previous step's swap-out writes
+        // (RAW: then the swap-ins wait for that D2H; older steps' D2H are done, synchronised
+        // above), and restore frees host slots at once, so this step's swap-out may overwrite
+        // a slot one of this step's swap-ins reads (WAR: then the D2H waits for the swap-ins,
+        // the reference's order, src/swap_engine.cpp:50-53)
+        bool raw = false;
+        for (int64_t j = 0; j < n_in && !raw; ++j)
+            raw = std::binary_search(T->prev_out_dst.begin(), T->prev_out_dst.end(), in_moves[j].src_slot);
         bool war = false;
         for (int64_t i = 0; i < n_out && !war; ++i)
             for (int64_t j = 0; j < n_in; ++j)
@@ -306,7 +317,7 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         }
         cuda_check(cudaEventRecord(T->gathered, cs), "event record");
         cuda_check(cudaStreamWaitEvent(xs, T->gathered, 0), "stream wait");
-        if (T->have_prev && n_in > 0) cuda_check(cudaStreamWaitEvent(xs, T->d2h_prev, 0), "stream wait");
+        if (raw) cuda_check(cudaStreamWaitEvent(xs, T->d2h_prev, 0), "stream wait");
         // 2. swap-in, layer by layer: H2D (batched) into staging, scatter, per-layer event
         T->any_in = n_in > 0;
         std::vector<void*> dst, src;
@@ -354,6 +365,9 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         if (T->mode_duplex && !war) {
             os = T->d2h;
             cuda_check(cudaStreamWaitEvent(os, T->gathered, 0), "stream wait");
+            // cross-step WAR: the previous step's swap-ins may still read a host slot this
+            // D2H reuses (restore frees host slots at once)
+            cuda_check(cudaStreamWaitEvent(os, T->done_p[par ^ 1], 0), "stream wait");
         }
         if (n_out > 0) {
             dst.clear();
@@ -370,13 +384,14 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
                 if (r != PB_OK) fail(r, "swap-out stamp");
             }
         }
-        if (os != xs) {
-            cuda_check(cudaEventRecord(T->d2h_done, os), "event record");
-            cuda_check(cudaStreamWaitEvent(xs, T->d2h_done, 0), "stream wait");
-        }
+        // the D2H no longer joins the copy stream: the next step's swap-ins only wait for it
+        // on a real RAW hazard
+        cuda_check(cudaEventRecord(T->d2h_p[par], os), "event record");
+        T->prev_out_dst.clear();
         if (n_out > 0) {
             cuda_check(cudaEventRecord(T->d2h_prev, os), "event record");
-            T->have_prev = true;
+            for (int64_t i = 0; i < n_out; ++i) T->prev_out_dst.push_back(out_moves[i].dst_slot);
+            std::sort(T->prev_out_dst.begin(), T->prev_out_dst.end());
         }
         cuda_check(cudaEventRecord(T->done_p[par], xs), "event record");
         cuda_check(cudaEventRecord(T->done, xs), "event record");
@@ -402,6 +417,7 @@ pb_status pb_swap_sync(pb_kv_tier* T) {
     return guarded([&] {
         if (!T) fail(PB_ERR_ERROR, "null tier");
         cuda_check(cudaEventSynchronize(T->done), "swap sync");
+        for (int b = 0; b < 2; ++b) cuda_check(cudaEventSynchronize(T->d2h_p[b]), "swap sync");
     });
 }
 

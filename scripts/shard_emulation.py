@@ -30,7 +30,7 @@ dev = torch.device("cuda", 0)
 stream = torch.cuda.current_stream()
 rows = []
 base = None
-for world in (1, 2, 4, 8):
+for world in [int(x) for x in os.environ.get("WORLDS", "1,2,4,8").split(",")]:
     shape = shard_shape(w.shape(), 0, world)
     pool = w.n_slots * w.chunk * shape.n_kv_head * w.head_size
     ks = [torch.empty(pool, dtype=torch.bfloat16, device=dev) for _ in range(n_layer)]

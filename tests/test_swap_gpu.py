@@ -126,3 +126,33 @@ def test_host_slot_hazards_across_and_within_steps(cuda):
         assert np.array_equal(kn[l, 9], k0[l, 2]) and np.array_equal(vn[l, 9], v0[l, 2])
         assert np.array_equal(kn[l, 10], old3[l, 0]) and np.array_equal(vn[l, 10], old3[l, 1])
         assert np.array_equal(host[3, l, 0], k0[l, 4]) and np.array_equal(host[3, l, 1], v0[l, 4])
+
+
+def test_cross_step_war_on_a_freed_host_slot(cuda):
+    """The D2H no longer joins the copy stream, so a step's swap-out could race the previous
+    step's swap-in from the same host slot (restore frees it at once and the next eviction may
+    reuse it).  Step 1 swaps host slot 5 in; step 2, issued right away with no layer wait on the
+    compute stream, swaps a device slot out to host slot 5: step 1 must still read the OLD bytes."""
+    torch = cuda
+    L, n_slots, page = 8, 16, 1 << 16
+    k, v = _pools(torch, L, n_slots, page, 6)
+    k0, v0 = k.cpu().numpy().copy(), v.cpu().numpy().copy()
+    tier = KvTier(L, 8, page, 8)
+    host = tier.host_view().reshape(8, L, 2, page)
+    rng = np.random.default_rng(7)
+    host[:] = rng.integers(0, 256, size=host.shape, dtype=np.uint8)
+    old = host.copy()
+    cs, xs = torch.cuda.Stream(), torch.cuda.Stream()
+    stride = n_slots * page
+    ins = [(c, h, 8 + h) for c, h in enumerate(range(8))]  # every host slot -> device 8..15
+    tier.step(k.data_ptr(), v.data_ptr(), stride, [], ins, cs.cuda_stream, xs.cuda_stream)
+    tier.step(k.data_ptr(), v.data_ptr(), stride, [(9, 1, 5)], [], cs.cuda_stream, xs.cuda_stream)
+    for l in range(L):
+        tier.wait_layer(l, cs.cuda_stream)
+    tier.sync()
+    torch.cuda.synchronize()
+    kn, vn = k.cpu().numpy(), v.cpu().numpy()
+    for l in range(L):
+        for h in range(8):
+            assert np.array_equal(kn[l, 8 + h], old[h, l, 0]) and np.array_equal(vn[l, 8 + h], old[h, l, 1])
+        assert np.array_equal(host[5, l, 0], k0[l, 1]) and np.array_equal(host[5, l, 1], v0[l, 1])
