@@ -4,9 +4,10 @@
 //   * swap-in is issued layer by layer (layer l of every chunk before layer l+1); an event per
 //     layer lets the compute stream start layer l's attention as soon as its pages landed
 //     (the LayerDependencyAuditor rule of src/event_log.cpp:90-118);
-//   * swap-out (D2H) runs on its own stream, concurrently with the swap-ins: measured faster
-//     on B200 than the reference's order (swap-out queued behind the step's swap-ins,
-//     schedule_swap_out_start, :50-53), which PB_SWAP_DUPLEX=0 restores;
+//   * swap-out (D2H) follows the step's swap-ins, as in the reference's order
+//     (schedule_swap_out_start, :50-53), but on its own stream: the next
+//     step's swap-ins and attention do not queue behind it (PB_SWAP_DUPLEX=0 puts it on the
+//     copy stream, =1 runs it concurrently with the swap-ins);
 //   * swap-in is a batched H2D into staging plus a scatter kernel per layer, or with
 //     PB_SWAP_IN=zc one zero-copy kernel per layer reading the mapped pinned tier;
 //   * the swap-out GATHER (device pages -> contiguous staging) runs first, on the compute
@@ -131,6 +132,15 @@ int n_sms() {
 // runtime refuses the batch.
 void copy_batch(std::vector<void*>& dst, std::vector<void*>& src, std::vector<size_t>& sizes, cudaStream_t st) {
     if (dst.empty()) return;
+    static const int use_batch = [] { // profiling knob: 0 = one cudaMemcpyAsync per piece
+        const char* e = std::getenv("PB_SWAP_BATCH");
+        return e ? std::atoi(e) : 1;
+    }();
+    if (!use_batch) {
+        for (size_t i = 0; i < dst.size(); ++i)
+            cuda_check(cudaMemcpyAsync(dst[i], src[i], sizes[i], cudaMemcpyDefault, st), "swap copy");
+        return;
+    }
     cudaMemcpyAttributes attr{};
     attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
     size_t attr_idx = 0, fail_idx = 0;
@@ -167,7 +177,7 @@ struct pb_kv_tier {
     int mode_zc = 0, mode_duplex = 0;
     int layer_block = 1;           // staged swap-in: layers per H2D piece (larger pieces, coarser events)
     pb_event_log* log = nullptr;   // optional: stamps SWAP_IN_LAYER / SWAP_OUT
-    cudaEvent_t gathered = nullptr, done = nullptr;
+    cudaEvent_t gathered = nullptr, done = nullptr, in_done = nullptr;
     std::vector<cudaEvent_t> layer_ready;
     bool any_in = false;
     int64_t chunk_bytes() const { return static_cast<int64_t>(n_layer) * 2 * page_bytes; }
@@ -215,11 +225,16 @@ pb_status pb_tier_create(int32_t n_layer, int32_t host_slots, int64_t page_bytes
         const char* m = std::getenv("PB_SWAP_IN");
         T->mode_zc = T->host_dev && m && std::string(m) == "zc"; // staged measured faster
         const char* dx = std::getenv("PB_SWAP_DUPLEX");
-        T->mode_duplex = !(dx && std::atoi(dx) == 0); // measured faster on B200 (profiles/)
+        // 0: D2H queued behind the swap-ins on the copy stream (the reference's order);
+        // 1: D2H concurrent with the swap-ins on its own stream; 2 (default): on its own stream
+        // after this step's swap-ins, so the swap-ins (on the attention's critical path) get
+        // the link alone and the D2H overlaps the following steps (measured, profiles/)
+        T->mode_duplex = dx ? std::atoi(dx) : 2;
         const char* lb = std::getenv("PB_SWAP_LB");
         T->layer_block = std::max(1, std::min(n_layer, lb ? std::atoi(lb) : kDefaultLayerBlock));
         cuda_check(cudaStreamCreateWithFlags(&T->d2h, cudaStreamNonBlocking), "d2h stream");
         cuda_check(cudaEventCreateWithFlags(&T->gathered, cudaEventDisableTiming), "event");
+        cuda_check(cudaEventCreateWithFlags(&T->in_done, cudaEventDisableTiming), "event");
         cuda_check(cudaEventCreateWithFlags(&T->done, cudaEventDisableTiming), "event");
         T->layer_ready.resize(static_cast<size_t>(n_layer));
         for (auto& e : T->layer_ready) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
@@ -251,6 +266,7 @@ void pb_tier_destroy(pb_kv_tier* T) {
         cudaStreamDestroy(T->d2h);
     }
     if (T->gathered) cudaEventDestroy(T->gathered);
+    if (T->in_done) cudaEventDestroy(T->in_done);
     if (T->done) cudaEventDestroy(T->done);
     for (auto e : T->layer_ready) cudaEventDestroy(e);
     delete T;
@@ -278,7 +294,6 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         const int par = T->par;
         T->par ^= 1;
         cuda_check(cudaEventSynchronize(T->done_p[par]), "swap step ordering");
-        cuda_check(cudaEventSynchronize(T->d2h_p[par]), "swap step ordering");
         int32_t* h_slots = T->h_slots[par];
         int32_t* d_slots = T->d_slots[par];
         uint8_t* stage_out = T->stage_out[par];
@@ -306,8 +321,11 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         const int64_t pb = T->page_bytes;
         auto* kp = static_cast<uint8_t*>(k_pool);
         auto* vp = static_cast<uint8_t*>(v_pool);
-        // 1. swap-out gather on the compute stream, before any same-step write to those slots
+        // 1. swap-out gather on the compute stream, before any same-step write to those slots;
+        // stage_out[par] is free once the D2H of two steps ago is done (a stream wait, so the
+        // host does not block on a D2H that may still run under later steps' attention)
         if (n_out > 0) {
+            cuda_check(cudaStreamWaitEvent(cs, T->d2h_p[par], 0), "stream wait");
             const int64_t jobs = n_out * T->n_layer * 2;
             const int grid = static_cast<int>(std::min<int64_t>(jobs, n_sms() * 8));
             swap_gather_kernel<<<grid, 256, 0, cs>>>(kp, vp, layer_stride, pb, d_slots, static_cast<int32_t>(n_out),
@@ -365,6 +383,10 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         if (T->mode_duplex && !war) {
             os = T->d2h;
             cuda_check(cudaStreamWaitEvent(os, T->gathered, 0), "stream wait");
+            if (T->mode_duplex == 2 && n_in > 0) {
+                cuda_check(cudaEventRecord(T->in_done, xs), "event record");
+                cuda_check(cudaStreamWaitEvent(os, T->in_done, 0), "stream wait");
+            }
             // cross-step WAR: the previous step's swap-ins may still read a host slot this
             // D2H reuses (restore frees host slots at once)
             cuda_check(cudaStreamWaitEvent(os, T->done_p[par ^ 1], 0), "stream wait");

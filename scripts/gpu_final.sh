@@ -13,6 +13,7 @@ for c in 2 3; do timeout 600 python bench.py --config $c > gpurun_out/${T}_bench
 timeout 600 python bench.py --config 5 > gpurun_out/${T}_bench_cfg5.txt 2>&1
 timeout 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 1 --master-addr 127.0.0.1 --master-port 29511 \
   bench.py --gpus 1 --steps 3 --warmup 3 --layers 8 --no-cpu-baseline > gpurun_out/${T}_torchrun1.txt 2>&1
+timeout 300 python scripts/shard_emulation.py > gpurun_out/${T}_shard.txt 2>&1
 timeout 600 python scripts/bench_strawmen.py --contexts 256,1024,4096 --reps 10 --out gpurun_out/${T}_strawmen.json > gpurun_out/${T}_strawmen.txt 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:attn -c 40 --csv \
   --log-file gpurun_out/${T}_launches_cfg4.csv python bench.py --steps 1 --warmup 3 --layers 8 --no-cpu-baseline > /dev/null 2>&1
