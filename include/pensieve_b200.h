@@ -206,7 +206,11 @@ pb_status pb_fill_splitmix_unit(void* dst, int32_t dtype, int64_t n, uint64_t se
  *   2. swap-in per layer on copy_stream: batched H2D into staging, scatter kernel into the
  *      pools, event per layer (pb_swap_wait_layer = "attention of layer l may start",
  *      PAPER.md:617-619);
- *   3. swap-out D2H after the swap-ins on copy_stream (schedule_swap_out_start, :50-53).
+ *   3. swap-out D2H after this step's swap-ins (schedule_swap_out_start, :50-53), on the
+ *      tier's own stream so the next step's swap-ins and attention do not queue behind it.
+ *      Host-slot hazards across steps are ordered by events: a swap-in waits for the previous
+ *      step's D2H only if it reads a host slot that D2H writes, and a D2H waits for the
+ *      previous step's swap-ins.  pb_swap_sync waits for everything, D2H included.
  * Pools: k_pool / v_pool hold n_layer pools at layer_stride bytes apart, pages of
  * page_bytes.  Moves come from pb_cache_apply_evictions (device src -> host dst) and
  * pb_cache_restore (host src -> device dst). */
