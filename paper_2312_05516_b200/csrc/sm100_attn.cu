@@ -80,6 +80,9 @@ constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max gr
 #ifndef PB_MMA_POLL
 #define PB_MMA_POLL 0   // 1: MMA warp issues S(j+1) / PV_A(j) / PV_B(j) in readiness order
 #endif
+#ifndef PB_ABLATE_HOOKS
+#define PB_ABLATE_HOOKS 0
+#endif
 #ifndef PB_POLY_EVERY
 #define PB_POLY_EVERY 0 // one exp2 pair in N on the FMA pipe; 0 = all on MUFU (measured fastest, see profiles/)
 #endif
@@ -457,6 +460,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr int kCols = kBN / kHalves;        // S columns per thread per kv tile
         constexpr int kOCols = D / kHalves;         // O columns per thread (rescale, epilogue)
         const float sl2 = p.scale_log2;
+        // PB_ABLATE roofline experiments exist only in builds with -DPB_ABLATE_HOOKS=1
+        // (scripts/build_variants.sh); the production kernel carries no checks for them
+        const int ablate = PB_ABLATE_HOOKS ? p.ablate : 0;
         uint32_t n_o = 0;
         uint32_t c_t = 0;     // kv tiles processed by this group (S buffer / barrier phase)
         uint32_t kv_seen = 0; // kv tiles loaded for earlier items (V ring position)
@@ -495,7 +501,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 {
                     mbar_wait(&s.s_full[t][b], (c_t >> 1) & 1);
                     tc_fence_after();
-                    if (p.ablate == 1) { // profiling: tensor-core + pipeline bound (P left as S bits)
+                    if (ablate == 1) { // profiling: tensor-core + pipeline bound (P left as S bits)
                         tc_fence_before();
                         mbar_arrive(&s.p_full[t][b]);
                         l_run = 1.f;
@@ -550,7 +556,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     // exp2((s - max) * log2e / scale) on packed pairs (FFMA2 / FADD2) and MUFU
                     const float2 a = fma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
                     float2 e;
-                    if (p.ablate == 2) { // profiling: no exponentials
+                    if (ablate == 2) { // profiling: no exponentials
                         e = a;
                     } else if (PB_POLY_EVERY > 0 && ((c >> 1) % (PB_POLY_EVERY > 0 ? PB_POLY_EVERY : 1)) ==
                                                         PB_POLY_EVERY - 1) {
@@ -565,7 +571,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // P (bf16) over the first kBN/2 columns of this S buffer (this half's share).
                 // Safe against the other half's S columns: both halves loaded their S before
                 // the max exchange above.
-                if (p.ablate != 5) {
+                if (ablate != 5) {
                     if constexpr (kCols == 64) tmem_st32(t_lane + col_s, *reinterpret_cast<uint32_t(*)[32]>(pk));
                     else dtc::tmem_st16(t_lane + col_s + hf * (kCols / 2), *reinterpret_cast<uint32_t(*)[16]>(pk));
                 }
