@@ -86,6 +86,24 @@ def test_bf16_random_ragged_batches(gh, oracle, n_head, n_kv, d, flags):
         assert ok, (trial, err, plan.stats())
 
 
+@pytest.mark.parametrize("n_head,n_kv,d", [(16, 1, 128), (48, 3, 128), (6, 2, 128), (10, 2, 128), (32, 1, 128),
+                                          (12, 4, 64)])
+def test_bf16_uncommon_group_sizes(gh, oracle, n_head, n_kv, d):
+    """GQA groups outside the configs: 16 (the decode kernel's widest N), non-powers of two
+    (3, 5: the tile packs 126 / 125 of 128 rows, decode pads N), and 32 (beyond the tensor-core
+    decode path) -- every head must still read kv head h / group (src/attention.cpp:92)."""
+    rng = SplitMix64(7000 + n_head * 10 + n_kv + d)
+    for trial in range(3):
+        w = random_instance(rng, n_head, n_kv, d, 16, PB_BF16, 1 + rng.next() % 6, 1500,
+                            all_decode=(trial == 2), max_q=300)
+        q, k, v = gh.device_inputs(w)
+        got, plan = gh.run_plan(w, q, k, v)
+        st, want = oracle.attention(w.shape(), w.batch(), w.host_q(), w.host_pool("k"), w.host_pool("v"))
+        assert st == 0
+        ok, err = gh.bf16_close(got, want)
+        assert ok, (trial, err, plan.stats())
+
+
 @pytest.mark.parametrize("cfg", [2, 3, 4])
 def test_bf16_configs_sampled_spans(gh, oracle, cfg):
     """Full-size config run on the GPU; oracle on a sample of spans (longest prefill, longest
