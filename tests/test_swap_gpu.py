@@ -42,9 +42,13 @@ def test_swap_out_then_in_roundtrip(cuda):
             assert np.array_equal(kn[l, dd], k0[l, d]) and np.array_equal(vn[l, dd], v0[l, d])
 
 
-def test_same_step_slot_reuse_hazard(cuda):
+@pytest.mark.parametrize("d2h_mode", ["2", "1", "0"])  # D2H after / concurrent with / behind swap-ins
+@pytest.mark.parametrize("swap_in", ["staged", "zc"])
+def test_same_step_slot_reuse_hazard(cuda, monkeypatch, d2h_mode, swap_in):
     """A device slot vacated by swap-out is refilled by a swap-in in the SAME step (the LIFO
     reclaim makes this common): the host must get the old bytes, the device the new ones."""
+    monkeypatch.setenv("PB_SWAP_DUPLEX", d2h_mode)  # read when the tier is created
+    monkeypatch.setenv("PB_SWAP_IN", swap_in)
     torch = cuda
     L, n_slots, page = 4, 8, 4096
     k, v = _pools(torch, L, n_slots, page, 2)
@@ -95,11 +99,15 @@ def test_cache_moves_drive_the_engine(cuda):
         assert np.array_equal(kn[:, s], truth[c][0]) and np.array_equal(vn[:, s], truth[c][1])
 
 
-def test_host_slot_hazards_across_and_within_steps(cuda):
+@pytest.mark.parametrize("d2h_mode", ["2", "1", "0"])  # D2H after / concurrent with / behind swap-ins
+@pytest.mark.parametrize("swap_in", ["staged", "zc"])
+def test_host_slot_hazards_across_and_within_steps(cuda, monkeypatch, d2h_mode, swap_in):
     """Host-side hazards of the double-buffered engine: (a) a swap-in in step s+1 from the host
     slot step s swapped out to (RAW across steps, without a host sync in between) gets the
     swapped-out bytes; (b) in one step, a swap-in reading host slot X and a swap-out writing X
     (restore frees X at once, src/paged_kv_cache.cpp:190) -- the swap-in gets the OLD bytes."""
+    monkeypatch.setenv("PB_SWAP_DUPLEX", d2h_mode)  # read when the tier is created
+    monkeypatch.setenv("PB_SWAP_IN", swap_in)
     torch = cuda
     L, n_slots, page = 6, 16, 8192
     k, v = _pools(torch, L, n_slots, page, 4)
@@ -128,11 +136,15 @@ def test_host_slot_hazards_across_and_within_steps(cuda):
         assert np.array_equal(host[3, l, 0], k0[l, 4]) and np.array_equal(host[3, l, 1], v0[l, 4])
 
 
-def test_cross_step_war_on_a_freed_host_slot(cuda):
+@pytest.mark.parametrize("d2h_mode", ["2", "1", "0"])  # D2H after / concurrent with / behind swap-ins
+@pytest.mark.parametrize("swap_in", ["staged", "zc"])
+def test_cross_step_war_on_a_freed_host_slot(cuda, monkeypatch, d2h_mode, swap_in):
     """The D2H no longer joins the copy stream, so a step's swap-out could race the previous
     step's swap-in from the same host slot (restore frees it at once and the next eviction may
     reuse it).  Step 1 swaps host slot 5 in; step 2, issued right away with no layer wait on the
     compute stream, swaps a device slot out to host slot 5: step 1 must still read the OLD bytes."""
+    monkeypatch.setenv("PB_SWAP_DUPLEX", d2h_mode)  # read when the tier is created
+    monkeypatch.setenv("PB_SWAP_IN", swap_in)
     torch = cuda
     L, n_slots, page = 8, 16, 1 << 16
     k, v = _pools(torch, L, n_slots, page, 6)
