@@ -94,10 +94,13 @@ pb_status pb_attn_plan_create(const pb_attn_shape* shape, int32_t n_spans,
                               int64_t total_tokens, int32_t flags, pb_attn_plan** out);
 /* Copies the plan's descriptors to the device on `stream` (first call allocates). */
 pb_status pb_attn_plan_upload(pb_attn_plan* plan, void* stream);
-/* Device workspace bytes pb_attn_run needs (split-KV partials + work-queue counters).  The
- * counters are zeroed on first use of a workspace buffer and are self-resetting after
- * every launch, so one workspace serves a whole layer loop; it must not be shared by two
- * launches that can run at the same time (give each stream its own). */
+/* Device workspace bytes pb_attn_run needs (split-KV partials + work-queue tickets).  The
+ * tickets are zeroed on first use of a workspace buffer and are self-resetting after every
+ * launch, so one workspace serves a whole layer loop and may be shared by several plans run
+ * one after another; it must not be shared by two launches that can run at the same time
+ * (give each stream its own).  The split-KV arrival counters live in the plan's own
+ * descriptor buffer (zeroed by pb_attn_plan_upload), so runs of one plan are serialised:
+ * run a plan on one stream at a time. */
 size_t pb_attn_plan_workspace_bytes(const pb_attn_plan* plan);
 /* Plan statistics: out[0] prefill tiles, [1] decode units, [2] split spans,
  * [3] algorithmic flops (4*n_head*d*sum allowed), [4] algorithmic bytes, [5] total tokens,
@@ -197,6 +200,31 @@ pb_status pb_kv_append(const pb_attn_shape* shape, int32_t n_spans, const int64_
 pb_status pb_fill_splitmix_unit(void* dst, int32_t dtype, int64_t n, uint64_t seed,
                                 uint64_t first_draw, void* stream);
 
+/* ===================================================================== model byte arithmetic
+ * kvsim::ModelConfig (include/kvsim/model_config.hpp; src/model_config.cpp:13-68).
+ * chunk_bytes is per worker: kv_token_bytes * chunk_size / n_partitions (:36-40), i.e. the
+ * bytes one rank's pools / host tier hold for one chunk under pb_shard_shape; a tier built
+ * with page_bytes = chunk_size * (n_kv_head / n_partitions) * head_size * bytes_per_scalar has
+ * pb_tier_chunk_bytes == pb_model_chunk_bytes. */
+typedef struct pb_model_config {
+    int32_t n_layer, hidden, n_head, n_kv_head, head_size, bytes_per_scalar, n_partitions;
+} pb_model_config;
+pb_status pb_model_validate(const pb_model_config* model);                  /* validate, :13-27 */
+pb_status pb_model_kv_token_bytes(const pb_model_config* model, uint64_t* out); /* :29-34 */
+pb_status pb_model_chunk_bytes(const pb_model_config* model, int32_t chunk_size, uint64_t* out); /* :36-40 */
+pb_status pb_model_preset(const char* name, pb_model_config* out);          /* preset, :48-68 */
+
+/* ===================================================================== multi-GPU shard
+ * KV-head sharding: rank r of `world` owns kv heads
+ * [r*n_kv/world, (r+1)*n_kv/world) and the query heads that read them, a contiguous block
+ * (head h reads kv head h / group, src/attention.cpp:91).  Spans, block tables and slots are
+ * identical on every rank; each rank builds its plan from the shard shape and runs it on its
+ * own device (one host thread or process per GPU; every pb_* call works on the CUDA device
+ * current on the calling thread, and a plan / tier belongs to the device current when it was
+ * uploaded / created).  Requires n_kv_head % world == 0 (src/model_config.cpp:25-26). */
+pb_status pb_shard_shape(const pb_attn_shape* full, int32_t rank, int32_t world, pb_attn_shape* out,
+                         int32_t* first_head, int32_t* first_kv_head);
+
 /* ===================================================================== CPU-tier swap engine
  * Pinned host tier [host_slot][layer][K|V][page] (one chunk = chunk_bytes contiguous,
  * src/model_config.cpp:36-40) and the ordered, layer-pipelined copies the reference only
@@ -208,9 +236,22 @@ pb_status pb_fill_splitmix_unit(void* dst, int32_t dtype, int64_t n, uint64_t se
  *      PAPER.md:617-619);
  *   3. swap-out D2H after this step's swap-ins (schedule_swap_out_start, :50-53), on the
  *      tier's own stream so the next step's swap-ins and attention do not queue behind it.
- *      Host-slot hazards across steps are ordered by events: a swap-in waits for the previous
- *      step's D2H only if it reads a host slot that D2H writes, and a D2H waits for the
- *      previous step's swap-ins.  pb_swap_sync waits for everything, D2H included.
+ *      Host-slot hazards across steps are ordered by events: a swap-in waits for the newest
+ *      D2H still in flight that writes the host slot it reads (any earlier step, not only
+ *      the previous one), and a D2H waits for the previous step's swap-ins.  pb_swap_sync
+ *      waits for everything, D2H included.
+ * Within one step the moves follow the scheduler's order: every eviction precedes every
+ * restore.  So
+ *   * a chunk swapped out and restored in the same step (out dst == in src, same chunk id)
+ *     is restored device-to-device from the swap-out staging, and its D2H is skipped (the
+ *     host copy is dead: restore frees the host slot);
+ *   * an out-move whose host slot a LATER out-move of the same step also writes is dead (its
+ *     chunk was dropped from the host in between) and is skipped, so no two copies of one
+ *     batch write the same host slot;
+ *   * an out-move writing a host slot a restore of a DIFFERENT chunk reads (restore freed
+ *     it) is a write-after-read: that D2H waits for the step's swap-ins.
+ * A chunk restored and then evicted again in one step is not representable; callers net it
+ * out (pb_sched never produces it).
  * Pools: k_pool / v_pool hold n_layer pools at layer_stride bytes apart, pages of
  * page_bytes.  Moves come from pb_cache_apply_evictions (device src -> host dst) and
  * pb_cache_restore (host src -> device dst). */
@@ -256,6 +297,22 @@ pb_status pb_swap_step(pb_kv_tier* tier, void* k_pool, void* v_pool, int64_t lay
                        const pb_slot_move* out_moves, int64_t n_out, const pb_slot_move* in_moves,
                        int64_t n_in, void* compute_stream, void* copy_stream);
 pb_status pb_swap_wait_layer(pb_kv_tier* tier, int32_t layer, void* compute_stream);
+/* Transfer policy (explicit, per tier; the defaults are the measured best on B200 and no
+ * environment variable changes them):
+ *   swap_in: PB_SWAP_IN_STAGED (default: batched H2D pieces into device staging + a scatter
+ *            kernel) or PB_SWAP_IN_ZERO_COPY (one kernel per layer reading the mapped pinned
+ *            tier);
+ *   d2h:     PB_D2H_AFTER_SWAP_IN (default: own stream, after this step's swap-ins),
+ *            PB_D2H_CONCURRENT (own stream, concurrent with the swap-ins unless a host slot
+ *            hazard orders it) or PB_D2H_ON_COPY_STREAM (queued behind the swap-ins on
+ *            copy_stream, the reference's literal order);
+ *   layers_per_piece: layers per swap-in H2D piece, 1..n_layer (default 8; 0 keeps it). */
+#define PB_SWAP_IN_STAGED 0
+#define PB_SWAP_IN_ZERO_COPY 1
+#define PB_D2H_ON_COPY_STREAM 0
+#define PB_D2H_CONCURRENT 1
+#define PB_D2H_AFTER_SWAP_IN 2
+pb_status pb_tier_set_policy(pb_kv_tier* tier, int32_t swap_in, int32_t d2h, int32_t layers_per_piece);
 pb_status pb_swap_sync(pb_kv_tier* tier);
 /* Attach (or detach with NULL) an event log to the tier's transfers. */
 pb_status pb_tier_set_event_log(pb_kv_tier* tier, pb_event_log* log);

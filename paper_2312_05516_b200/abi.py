@@ -14,11 +14,6 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 SO_PATH = os.path.join(HERE, "libpensieve_b200.so")
-# profiling experiments only: PB_LIB names an alternate in-tree build of the same library
-# (scripts/build_variants.sh); the product always loads SO_PATH
-if os.environ.get("PB_LIB"):
-    _v = os.environ["PB_LIB"]
-    SO_PATH = os.path.join(HERE, "variants", _v if _v.endswith(".so") else _v + ".so")
 
 PB_F32 = 0
 PB_BF16 = 1
@@ -309,6 +304,57 @@ def fill_unit(dst: int, dtype: int, n: int, seed: int, first_draw: int,
     check(lib.pb_fill_splitmix_unit(dst, dtype, n, seed, first_draw, stream))
 
 
+# ============================================================================ model bytes, shards
+class ModelConfig(ctypes.Structure):
+    """pb_model_config: kvsim::ModelConfig's integer fields (include/kvsim/model_config.hpp)."""
+    _fields_ = [("n_layer", _I32), ("hidden", _I32), ("n_head", _I32), ("n_kv_head", _I32),
+                ("head_size", _I32), ("bytes_per_scalar", _I32), ("n_partitions", _I32)]
+
+
+_MODEL_SIGS = {
+    "pb_model_validate": (_I32, [ctypes.POINTER(ModelConfig)]),
+    "pb_model_kv_token_bytes": (_I32, [ctypes.POINTER(ModelConfig), ctypes.POINTER(ctypes.c_uint64)]),
+    "pb_model_chunk_bytes": (_I32, [ctypes.POINTER(ModelConfig), _I32, ctypes.POINTER(ctypes.c_uint64)]),
+    "pb_model_preset": (_I32, [ctypes.c_char_p, ctypes.POINTER(ModelConfig)]),
+    "pb_shard_shape": (_I32, [_SHP, _I32, _I32, _SHP, ctypes.POINTER(_I32), ctypes.POINTER(_I32)]),
+}
+for _name, (_res, _args) in _MODEL_SIGS.items():
+    _f = getattr(lib, _name)
+    _f.restype = _res
+    _f.argtypes = _args
+_SIGS.update(_MODEL_SIGS)
+
+
+def model_preset(name: str) -> ModelConfig:
+    m = ModelConfig()
+    check(lib.pb_model_preset(name.encode(), ctypes.byref(m)))
+    return m
+
+
+def model_validate(m: ModelConfig) -> None:
+    check(lib.pb_model_validate(ctypes.byref(m)))
+
+
+def kv_token_bytes(m: ModelConfig) -> int:
+    out = ctypes.c_uint64()
+    check(lib.pb_model_kv_token_bytes(ctypes.byref(m), ctypes.byref(out)))
+    return int(out.value)
+
+
+def chunk_bytes(m: ModelConfig, chunk_size: int) -> int:
+    out = ctypes.c_uint64()
+    check(lib.pb_model_chunk_bytes(ctypes.byref(m), chunk_size, ctypes.byref(out)))
+    return int(out.value)
+
+
+def shard_shape(shape: AttnShape, rank: int, world: int):
+    """pb_shard_shape: (shard AttnShape, first query head, first kv head) of rank / world."""
+    out, h0, k0 = AttnShape(), _I32(), _I32()
+    check(lib.pb_shard_shape(ctypes.byref(shape), rank, world, ctypes.byref(out), ctypes.byref(h0),
+                             ctypes.byref(k0)))
+    return out, int(h0.value), int(k0.value)
+
+
 # ============================================================================ KV bookkeeping
 class SlotMove(ctypes.Structure):
     _fields_ = [("chunk", ctypes.c_int64), ("src_slot", ctypes.c_int32), ("dst_slot", ctypes.c_int32)]
@@ -476,6 +522,7 @@ _TIER_SIGS = {
     "pb_swap_wait_layer": (_I32, [_P, _I32, _P]),
     "pb_swap_sync": (_I32, [_P]),
     "pb_tier_set_event_log": (_I32, [_P, _P]),
+    "pb_tier_set_policy": (_I32, [_P, _I32, _I32, _I32]),
     "pb_evlog_create": (_I32, [_I64, ctypes.POINTER(_P)]),
     "pb_evlog_destroy": (None, [_P]),
     "pb_evlog_mark": (_I32, [_P, _I32, _I32, _I64, _P]),
@@ -540,6 +587,10 @@ class EventLog:
         check(lib.pb_evlog_reset(self._h))
 
 
+PB_SWAP_IN_STAGED, PB_SWAP_IN_ZERO_COPY = 0, 1
+PB_D2H_ON_COPY_STREAM, PB_D2H_CONCURRENT, PB_D2H_AFTER_SWAP_IN = 0, 1, 2
+
+
 class KvTier:
     """pb_kv_tier: pinned host tier + ordered, layer-pipelined swap copies."""
 
@@ -570,6 +621,11 @@ class KvTier:
         om, im = _moves_array(out_moves), _moves_array(in_moves)
         check(lib.pb_swap_step(self._h, k_pool, v_pool, layer_stride, om, len(out_moves), im, len(in_moves),
                                compute_stream, copy_stream))
+
+    def set_policy(self, swap_in: int = PB_SWAP_IN_STAGED, d2h: int = PB_D2H_AFTER_SWAP_IN,
+                   layers_per_piece: int = 0) -> None:
+        """pb_tier_set_policy: transfer method / D2H ordering (defaults are the measured best)."""
+        check(lib.pb_tier_set_policy(self._h, swap_in, d2h, layers_per_piece))
 
     def set_event_log(self, log: Optional["EventLog"]) -> None:
         self._log = log

@@ -21,6 +21,25 @@ std::atomic<uint64_t> g_launches{0};
 void set_last_error(const std::string& msg) { t_last_error = msg; }
 void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
 
+int device_sms() {
+    static std::once_flag once[kMaxDevices];
+    static int sms[kMaxDevices];
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= kMaxDevices) {
+        cudaGetLastError();
+        return 148;
+    }
+    std::call_once(once[dev], [&] {
+        int n = 0;
+        if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) {
+            cudaGetLastError();
+            n = 148;
+        }
+        sms[dev] = n;
+    });
+    return sms[dev];
+}
+
 void plan_validate_with_q(const pb_attn_shape& s, int32_t n_spans, const int64_t* qs,
                           const int64_t* ql, const int64_t* cl, const int64_t* co,
                           const int32_t* bt, const int64_t* bt_off, int64_t total_tokens,

@@ -3,8 +3,9 @@
 // span s (row query_start + i of the new K/V rows) goes to position causal_offset + i, i.e.
 // page block_table[pos / chunk], row pos % chunk, every kv head.  In the fused launch every
 // CTA writes a share of the rows, then a grid-wide barrier orders those writes before any
-// CTA's TMA reads the pages (the launch is persistent with one CTA per SM, so all CTAs are
-// co-resident).
+// CTA's TMA reads the pages.  The barrier needs every CTA co-resident, so launches carrying
+// new rows are cooperative (launch_fused / launch_dt fall back to a separate row-write launch
+// when the runtime refuses a cooperative launch).
 #pragma once
 
 #include "attn_internal.hpp"

@@ -396,24 +396,12 @@ __global__ void __launch_bounds__(dec_warps<D, G>() * 32, 1)
     }
 }
 
-int g_dec_sms = 0;
-
 template <int D, int G>
 void launch_decode_t(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st) {
     const size_t smem = sizeof(DecWarp<D, G>) * dec_warps<D, G>() + 1024;
-    static bool attr = false;
-    if (!attr) {
-        cuda_check(cudaFuncSetAttribute(attn_decode_kernel<D, G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)),
-                   "cudaFuncSetAttribute(decode smem)");
-        attr = true;
-    }
-    if (g_dec_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_dec_sms, cudaDevAttrMultiProcessorCount, dev);
-    }
-    const int grid = std::max(1, std::min(g_dec_sms, (p.n_items + dec_warps<D, G>() - 1) / dec_warps<D, G>()));
+    static std::once_flag attr[kMaxDevices];
+    set_smem_once(attr, attn_decode_kernel<D, G>, smem, "cudaFuncSetAttribute(decode smem)");
+    const int grid = std::max(1, std::min(device_sms(), (p.n_items + dec_warps<D, G>() - 1) / dec_warps<D, G>()));
     attn_decode_kernel<D, G><<<grid, dec_warps<D, G>() * 32, smem, st>>>(maps[1], maps[2], p);
     cuda_check(cudaGetLastError(), "attn_decode launch");
     count_launch();
@@ -438,13 +426,8 @@ bool decode_supports(int head_size, int chunk, int group) {
 void launch_attn_decode(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens,
                         cudaStream_t stream) {
     if (p.n_items <= 0) return;
-    // GQA groups of 3..16 heads at d = 128 go to the tcgen05 decode kernel (attn_decode_tc.cu);
-    // PB_DECODE=simt keeps them here (profiling comparisons only)
-    static const bool force_simt = [] {
-        const char* e = std::getenv("PB_DECODE");
-        return e && std::string(e) == "simt";
-    }();
-    if (!force_simt && decode_tc_supports(shape.head_size, shape.chunk_size, p.group)) {
+    // GQA groups of 3..16 heads at d = 128 go to the tcgen05 decode kernel (attn_decode_tc.cu)
+    if (decode_tc_supports(shape.head_size, shape.chunk_size, p.group)) {
         launch_attn_decode_tc(p, shape, cache, total_tokens, stream);
         return;
     }

@@ -57,25 +57,42 @@ __global__ void __launch_bounds__(256) append_spans_kernel(const AttnParams p) {
                 static_cast<int>((gridDim.x * blockDim.x) >> 5));
 }
 
-int g_dt_sms = 0;
-
 template <int G>
 void launch_dt(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st) {
     const size_t smem = sizeof(DtSmem) + 1024;
-    static bool attr = false;
-    if (!attr) {
-        cuda_check(cudaFuncSetAttribute(attn_decode_tc_kernel<G>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)),
-                   "cudaFuncSetAttribute(decode tc smem)");
-        attr = true;
+    static std::once_flag attr[kMaxDevices];
+    set_smem_once(attr, attn_decode_tc_kernel<G>, smem, "cudaFuncSetAttribute(decode tc smem)");
+    const int grid = std::max(1, std::min(device_sms(), p.n_items));
+    if (!p.k_new) {
+        attn_decode_tc_kernel<G><<<grid, kDtThreads, smem, st>>>(maps[3], maps[1], maps[2], p);
+        cuda_check(cudaGetLastError(), "attn_decode_tc launch");
+        count_launch();
+        return;
     }
-    if (g_dt_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_dt_sms, cudaDevAttrMultiProcessorCount, dev);
+    // fused append: its grid barrier needs co-resident CTAs (cooperative launch), else the
+    // rows get their own launch first (see launch_fused, sm100_attn.cu)
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kDtThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute coop{};
+    coop.id = cudaLaunchAttributeCooperative;
+    coop.val.cooperative = 1;
+    cfg.attrs = &coop;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_decode_tc_kernel<G>, maps[3], maps[1], maps[2], p);
+    if (e == cudaSuccess) {
+        count_launch();
+        return;
     }
-    const int grid = std::max(1, std::min(g_dt_sms, p.n_items));
-    attn_decode_tc_kernel<G><<<grid, kDtThreads, smem, st>>>(maps[3], maps[1], maps[2], p);
+    if (e != cudaErrorCooperativeLaunchTooLarge) cuda_check(e, "attn_decode_tc cooperative launch");
+    cudaGetLastError();
+    launch_append_spans(p, st);
+    AttnParams q = p;
+    q.k_new = nullptr;
+    q.v_new = nullptr;
+    attn_decode_tc_kernel<G><<<grid, kDtThreads, smem, st>>>(maps[3], maps[1], maps[2], q);
     cuda_check(cudaGetLastError(), "attn_decode_tc launch");
     count_launch();
 }

@@ -60,7 +60,6 @@ struct AttnParams {
     // [3] fused: retired CTAs, [4] next tcgen05 decode unit, [5] stand-alone decode: retired
     // CTAs, [6] fused-append grid barrier arrivals, [7] its generation
     int32_t* work_counter;
-    int32_t ablate;          // profiling only (PB_ABLATE): 1 skip softmax math, 2 skip exp
     // fused launch: decode units next to the tile items (items / n_items)
     const WorkItem* dec_items;
     int32_t n_dec_items;

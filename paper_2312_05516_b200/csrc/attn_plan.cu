@@ -55,6 +55,8 @@ struct pb_attn_plan {
     void* d_buf = nullptr;
     size_t d_bytes = 0;
     size_t off_bt = 0, off_simt = 0, off_tc = 0, off_dec = 0;
+    size_t off_ctr = 0; // split-group arrival counters: plan-private (zeroed by the upload,
+                        // self-resetting), so plans sharing one workspace cannot clobber them
     bool uploaded = false;
     void* last_workspace = nullptr;
     Sm100Cache sm100;
@@ -64,19 +66,7 @@ namespace {
 
 size_t align_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
 
-int sm_count() {
-    static int n = 0;
-    if (n == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) {
-            cudaGetLastError(); // no device (host-only plan building): B200's count
-            n = 148;
-        }
-    }
-    return n;
-}
+int sm_count() { return device_sms(); }
 
 int dtype_bytes(int dtype) { return dtype == PB_F32 ? 4 : 2; }
 
@@ -124,7 +114,6 @@ void validate(const pb_attn_shape& s, int32_t n_spans, const int64_t* qs, const 
 // balance), never more than 64 pages (the decode kernel caches a unit's block-table slice in
 // two registers per lane) and never fewer than 8.
 constexpr int kDecodeUnitsTarget = 4096;
-constexpr int kDecodeUnitsTargetTc = 800; // measured: fewer, longer units (fewer merges) stream faster
 
 void build_work(pb_attn_plan& P) {
     const pb_attn_shape& s = P.shape;
@@ -133,11 +122,7 @@ void build_work(pb_attn_plan& P) {
                     sm100_supports(s.head_size, s.chunk_size, g);
     // SIMT tiles: blocks of tokens, ~16 rows per warp-pass
     const int simt_tokens = std::max(1, 32 / g);
-    static const int tile_half = [] { // profiling: one query tile per item instead of two
-        const char* e = std::getenv("PB_TILE_HALF");
-        return e ? std::atoi(e) : 0;
-    }();
-    const int tc_tokens = tc ? sm100_tile_tokens(g) / (tile_half ? 2 : 1) : 0;
+    const int tc_tokens = tc ? sm100_tile_tokens(g) : 0;
     P.decode_kernel = tc && (decode_supports(s.head_size, s.chunk_size, g) ||
                              decode_tc_supports(s.head_size, s.chunk_size, g));
     std::vector<std::pair<double, WorkItem>> tc_list, dec_list;
@@ -147,23 +132,16 @@ void build_work(pb_attn_plan& P) {
     // the tcgen05 decode kernel streams one unit per CTA (148 in flight): ~10 units per CTA,
     // 16..128 pages each; the SIMT kernel streams one unit per warp: ~kDecodeUnitsTarget units
     const bool dec_tc = P.decode_kernel && decode_tc_supports(s.head_size, s.chunk_size, g);
-    static const int64_t units_tc = [] { // profiling knob: decode units per launch (tcgen05 path)
-        const char* e = std::getenv("PB_DEC_UNITS");
-        return e ? std::max<int64_t>(1, std::atoll(e)) : static_cast<int64_t>(kDecodeUnitsTargetTc);
-    }();
     int64_t decode_pairs = 0;
     for (const SpanDev& sp : P.spans)
         if (sp.query_len == 1) decode_pairs += s.n_kv_head;
     // tcgen05 decode: a split span costs a partial write, an atomic ticket and a merge, which
     // measured slower than whole spans as soon as there is at least one (span, kv head) pair
     // per CTA (cfg3: 95% -> 99% of HBM; the config-5 steps: 52 -> 40 us); with fewer pairs,
-    // split to ~1.5 units per CTA (>= 16 pages each).  PB_DEC_UNITS (profiling) forces a
-    // unit-count target instead.
+    // split to ~1.5 units per CTA (>= 16 pages each).
     const int64_t sms = sm_count();
     int split_pages;
-    if (dec_tc && std::getenv("PB_DEC_UNITS"))
-        split_pages = static_cast<int>(std::max<int64_t>(16, std::min<int64_t>(128, decode_pages / units_tc)));
-    else if (dec_tc)
+    if (dec_tc)
         split_pages = decode_pairs >= sms
                           ? (1 << 24) // no split
                           : static_cast<int>(std::max<int64_t>(16, (2 * decode_pages + 3 * sms - 1) / (3 * sms)));
@@ -244,22 +222,14 @@ void build_work(pb_attn_plan& P) {
     // One launch for the whole batch: when both kinds exist and the decode units fit the
     // tensor-core decode path, they join the tile kernel's work list (the fused kernel serves
     // both; HBM-bound units fill SMs next to tensor-bound tiles).
-    static const bool fuse_all = [] { // profiling: decode-only batches through the fused kernel
-        const char* e = std::getenv("PB_FUSE_DECODE_ONLY");
-        return e && std::atoi(e) != 0;
-    }();
-    P.fused = dec_tc && (!tc_list.empty() || fuse_all) && !dec_list.empty() &&
+    P.fused = dec_tc && !tc_list.empty() && !dec_list.empty() &&
               !(P.flags & PB_PLAN_SEPARATE_DECODE);
     // Heavy items first so the persistent CTAs finish together (LPT order).
     auto lpt = [](auto& v) {
         std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
     };
     lpt(dec_list);
-    static const int tile_order = [] { // 1 (default): items of one (span, kv head) together
-        const char* e = std::getenv("PB_TILE_ORDER");
-        return e ? std::atoi(e) : 1;
-    }();
-    if (tile_order == 1 && !tc_list.empty()) {
+    if (!tc_list.empty()) {
         // The query blocks of one (span, kv head) stream the same K/V pages: keeping them
         // adjacent in the queue lets concurrently running CTAs share those pages through L2.
         // Groups go heaviest first (by their heaviest item), items heaviest first inside.
@@ -349,7 +319,8 @@ pb_status pb_attn_plan_upload(pb_attn_plan* P, void* stream) {
         P->off_simt = align_up(P->off_bt + sizeof(int32_t) * P->bt.size(), 256);
         P->off_tc = align_up(P->off_simt + sizeof(WorkItem) * P->simt_items.size(), 256);
         P->off_dec = align_up(P->off_tc + sizeof(WorkItem) * P->tc_items.size(), 256);
-        const size_t total = std::max<size_t>(256, P->off_dec + sizeof(WorkItem) * P->decode_items.size());
+        P->off_ctr = align_up(P->off_dec + sizeof(WorkItem) * P->decode_items.size(), 256);
+        const size_t total = std::max<size_t>(256, P->off_ctr + sizeof(int32_t) * static_cast<size_t>(P->n_groups));
         if (P->d_bytes < total) {
             if (P->d_buf) cudaFree(P->d_buf);
             P->d_buf = nullptr;
@@ -388,8 +359,7 @@ pb_status pb_attn_plan_upload(pb_attn_plan* P, void* stream) {
 size_t pb_attn_plan_workspace_bytes(const pb_attn_plan* P) {
     if (!P) return 0;
     const size_t g = static_cast<size_t>(P->group);
-    size_t b = 256; // work counter + padding
-    b += align_up(sizeof(int32_t) * static_cast<size_t>(P->n_groups), 256);
+    size_t b = 256; // work-queue tickets (self-resetting) + padding
     b += align_up(sizeof(float) * 2 * g * static_cast<size_t>(P->n_parts), 256);
     b += align_up(sizeof(float) * g * P->shape.head_size * static_cast<size_t>(P->n_parts), 256);
     return b;
@@ -431,6 +401,7 @@ static AttnParams make_params(pb_attn_plan* P, const void* q, const void* k, con
     auto* base = static_cast<uint8_t*>(P->d_buf);
     p.spans = reinterpret_cast<const SpanDev*>(base);
     p.block_tables = reinterpret_cast<const int32_t*>(base + P->off_bt);
+    p.counters = reinterpret_cast<int32_t*>(base + P->off_ctr);
     p.q = q;
     p.k_pages = k;
     p.v_pages = v;
@@ -440,8 +411,6 @@ static AttnParams make_params(pb_attn_plan* P, const void* q, const void* k, con
         const size_t g = static_cast<size_t>(P->group);
         p.work_counter = reinterpret_cast<int32_t*>(w);
         size_t off = 256;
-        p.counters = reinterpret_cast<int32_t*>(w + off);
-        off += align_up(sizeof(int32_t) * static_cast<size_t>(P->n_groups), 256);
         p.part_ml = reinterpret_cast<float*>(w + off);
         off += align_up(sizeof(float) * 2 * g * static_cast<size_t>(P->n_parts), 256);
         p.part_o = reinterpret_cast<float*>(w + off);
@@ -462,27 +431,16 @@ static void run_impl(pb_attn_plan* P, const void* q, const void* k_pages, const 
             fail(PB_ERR_ERROR, "workspace required");
         cudaStream_t st = as_stream(stream);
         AttnParams p = make_params(P, q, k_pages, v_pages, out, workspace);
-        static const int ablate = [] {
-            const char* e = std::getenv("PB_ABLATE");
-            return e ? std::atoi(e) : 0;
-        }();
-        p.ablate = ablate;
         p.trace = static_cast<unsigned long long*>(P->trace);
-        // profiling only (PB_ONLY): 1 = run only the tile kernel, 2 = only the decode kernel
-        static const int only = [] {
-            const char* e = std::getenv("PB_ONLY");
-            return e ? std::atoi(e) : 0;
-        }();
         if (workspace && workspace != P->last_workspace) {
-            // counters are self-resetting; zero them once per workspace buffer
-            cuda_check(cudaMemsetAsync(workspace, 0, 256 + align_up(sizeof(int32_t) * P->n_groups, 256), st),
-                       "workspace init");
+            // the queue tickets are self-resetting; zero them once per workspace buffer
+            cuda_check(cudaMemsetAsync(workspace, 0, 256, st), "workspace init");
             P->last_workspace = workspace;
         }
         if (k_new) {
             // fused append: inside the (single) attention launch when there is one, else a
             // stand-alone row-write launch first (the same rows, the same addressing)
-            const bool single = only == 0 && P->simt_items.empty() && P->shape.dtype == PB_BF16 &&
+            const bool single = P->simt_items.empty() && P->shape.dtype == PB_BF16 &&
                                 (P->fused || P->decode_items.empty() ||
                                  (P->tc_items.empty() && decode_tc_supports(P->shape.head_size, P->shape.chunk_size,
                                                                             P->group)));
@@ -506,17 +464,13 @@ static void run_impl(pb_attn_plan* P, const void* q, const void* k_pages, const 
         // is forked onto a side stream so its persistent CTAs take SMs as soon as tile CTAs
         // retire (the tile kernel's tail) and the two bottlenecks overlap; joined back before
         // pb_attn_run's stream continues.
-        if (P->fused && only == 0) {
+        if (P->fused) {
             // one launch: tile items and decode units from two queues (sm100_attn.cu)
-            static const double cta_scale_env = [] {
-                const char* e = std::getenv("PB_DEC_CTA_SCALE"); // profiling knob
-                return e ? std::atof(e) : 0.0;
-            }();
             // A decode CTA next to tensor-bound tiles streams slower than 1/148 of HBM, so a
             // small decode share is under-estimated: double it below 25% (measured: cfg4 at an
             // 8-way kv-head shard 92 -> 83 us per layer, unchanged at N = 1; cfg2, where decode
             // is most of the launch, is best unscaled, profiles/r1_variants.md).
-            const double cta_scale = cta_scale_env > 0 ? cta_scale_env : (P->dec_share < 0.25 ? 2.0 : 1.0);
+            const double cta_scale = P->dec_share < 0.25 ? 2.0 : 1.0;
             AttnParams pf = p;
             pf.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_tc);
             pf.n_items = static_cast<int32_t>(P->tc_items.size());
@@ -529,8 +483,8 @@ static void run_impl(pb_attn_plan* P, const void* q, const void* k_pages, const 
             launch_attn_sm100(pf, P->shape, P->sm100, P->total_tokens, st);
             return;
         }
-        const bool run_tc = !P->tc_items.empty() && only != 2;
-        const bool run_dec = !P->decode_items.empty() && only != 1;
+        const bool run_tc = !P->tc_items.empty();
+        const bool run_dec = !P->decode_items.empty();
         const bool both = run_tc && run_dec;
         cudaStream_t dst = st;
         if (both) {

@@ -24,16 +24,7 @@ namespace pb {
 
 namespace {
 
-int g_num_sms = 0;
-int num_sms() {
-    if (g_num_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-        if (g_num_sms <= 0) g_num_sms = 148;
-    }
-    return g_num_sms;
-}
+int num_sms() { return device_sms(); }
 
 // dst/src page index for item j = (layer l, page i)
 template <bool kGather>

@@ -7,6 +7,7 @@
 
 #include <atomic>
 #include <cstdint>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 
@@ -52,5 +53,32 @@ template <class F> pb_status guarded(F&& f) {
 }
 
 inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ---- per-device state (one host thread per GPU is the multi-GPU control plane)
+// Kernel attributes such as the dynamic shared-memory opt-in are per device, so they are set
+// once per (kernel, device) under std::call_once; SM counts are cached per device.
+constexpr int kMaxDevices = 64;
+
+inline int current_device() {
+    int dev = 0;
+    cuda_check(cudaGetDevice(&dev), "cudaGetDevice");
+    if (dev < 0 || dev >= kMaxDevices) fail(PB_ERR_UNSUPPORTED, "device ordinal out of range");
+    return dev;
+}
+
+// SM count of the current device (148 on B200).  With no usable device (host-only plan
+// building in the CPU container) the B200 count is returned.
+int device_sms();
+
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (kernel, device).  `flags` is the
+// per-kernel once-table (a function-local static in the launcher).
+template <class K>
+inline void set_smem_once(std::once_flag (&flags)[kMaxDevices], K kernel, size_t bytes, const char* what) {
+    const int dev = current_device();
+    std::call_once(flags[dev], [&] {
+        cuda_check(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)),
+                   what);
+    });
+}
 
 } // namespace pb

@@ -37,6 +37,7 @@
 
 #include <algorithm>
 #include <cstring>
+#include <mutex>
 
 namespace pb {
 
@@ -80,8 +81,8 @@ constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max gr
 #ifndef PB_MMA_POLL
 #define PB_MMA_POLL 0   // 1: MMA warp issues S(j+1) / PV_A(j) / PV_B(j) in readiness order
 #endif
-#ifndef PB_ABLATE_HOOKS
-#define PB_ABLATE_HOOKS 0
+#ifndef PB_ABLATE_MODE
+#define PB_ABLATE_MODE 0 // roofline ablations, separate builds only: 1 no softmax, 2 no exp2, 5 no P store
 #endif
 #ifndef PB_POLY_EVERY
 #define PB_POLY_EVERY 0 // one exp2 pair in N on the FMA pipe; 0 = all on MUFU (measured fastest, see profiles/)
@@ -460,9 +461,9 @@ __global__ void __launch_bounds__(kThreads, 1)
         constexpr int kCols = kBN / kHalves;        // S columns per thread per kv tile
         constexpr int kOCols = D / kHalves;         // O columns per thread (rescale, epilogue)
         const float sl2 = p.scale_log2;
-        // PB_ABLATE roofline experiments exist only in builds with -DPB_ABLATE_HOOKS=1
+        // roofline ablations exist only in builds with -DPB_ABLATE_MODE=n
         // (scripts/build_variants.sh); the production kernel carries no checks for them
-        const int ablate = PB_ABLATE_HOOKS ? p.ablate : 0;
+        constexpr int ablate = PB_ABLATE_MODE;
         uint32_t n_o = 0;
         uint32_t c_t = 0;     // kv tiles processed by this group (S buffer / barrier phase)
         uint32_t kv_seen = 0; // kv tiles loaded for earlier items (V ring position)
@@ -655,16 +656,19 @@ __global__ void __launch_bounds__(kThreads, 1)
 
 // ------------------------------------------------------------------ host side
 
-PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() { // a driver entry point: one per process
+    static std::once_flag once;
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
-    if (!fn) {
+    std::call_once(once, [] {
         void* f = nullptr;
         cudaDriverEntryPointQueryResult q{};
-        cuda_check(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q),
-                   "cudaGetDriverEntryPoint(cuTensorMapEncodeTiled)");
-        if (!f || q != cudaDriverEntryPointSuccess) fail(PB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
-        fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
-    }
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) == cudaSuccess &&
+            f && q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+        else
+            cudaGetLastError();
+    });
+    if (!fn) fail(PB_ERR_CUDA, "cuTensorMapEncodeTiled unavailable");
     return fn;
 }
 
@@ -680,25 +684,44 @@ void encode_3d(CUtensorMap* m, const void* ptr, uint64_t d0, uint64_t d1, uint64
     if (r != CUDA_SUCCESS) fail(PB_ERR_CUDA, "cuTensorMapEncodeTiled failed (" + std::to_string(static_cast<int>(r)) + ")");
 }
 
-int g_sms = 0;
-
 template <int D, int GD>
 void launch_fused(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st) {
     const size_t smem = std::max(sizeof(Smem<D>), sizeof(dtc::DtSmem)) + 1024;
-    static bool attr_set = false;
-    if (!attr_set) {
-        cuda_check(cudaFuncSetAttribute(attn_fused_sm100_kernel<D, GD>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                        static_cast<int>(smem)),
-                   "cudaFuncSetAttribute(fused smem)");
-        attr_set = true;
+    static std::once_flag attr[kMaxDevices];
+    set_smem_once(attr, attn_fused_sm100_kernel<D, GD>, smem, "cudaFuncSetAttribute(fused smem)");
+    const int grid = std::min(p.n_items + (D == 128 ? p.n_dec_items : 0), device_sms());
+    if (!p.k_new) {
+        attn_fused_sm100_kernel<D, GD><<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
+        cuda_check(cudaGetLastError(), "attn_fused_sm100 launch");
+        count_launch();
+        return;
     }
-    if (g_sms == 0) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+    // The fused append ends in a grid-wide barrier, so every CTA must be co-resident: a
+    // cooperative launch guarantees it (or refuses, e.g. under an MPS SM limit or next to a
+    // persistent kernel on another stream); when refused, the rows are written by their own
+    // launch first and the attention launch carries no barrier.
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(static_cast<unsigned>(grid));
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr_coop{};
+    attr_coop.id = cudaLaunchAttributeCooperative;
+    attr_coop.val.cooperative = 1;
+    cfg.attrs = &attr_coop;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_fused_sm100_kernel<D, GD>, maps[0], maps[1], maps[2], maps[3], p);
+    if (e == cudaSuccess) {
+        count_launch();
+        return;
     }
-    const int grid = std::min(p.n_items + (D == 128 ? p.n_dec_items : 0), g_sms);
-    attn_fused_sm100_kernel<D, GD><<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
+    if (e != cudaErrorCooperativeLaunchTooLarge) cuda_check(e, "attn_fused_sm100 cooperative launch");
+    cudaGetLastError();
+    launch_append_spans(p, st);
+    AttnParams q = p;
+    q.k_new = nullptr;
+    q.v_new = nullptr;
+    attn_fused_sm100_kernel<D, GD><<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], q);
     cuda_check(cudaGetLastError(), "attn_fused_sm100 launch");
     count_launch();
 }

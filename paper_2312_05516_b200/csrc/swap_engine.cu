@@ -6,17 +6,20 @@
 //     (the LayerDependencyAuditor rule of src/event_log.cpp:90-118);
 //   * swap-out (D2H) follows the step's swap-ins, as in the reference's order
 //     (schedule_swap_out_start, :50-53), but on its own stream: the next
-//     step's swap-ins and attention do not queue behind it (PB_SWAP_DUPLEX=0 puts it on the
-//     copy stream, =1 runs it concurrently with the swap-ins);
-//   * swap-in is a batched H2D into staging plus a scatter kernel per layer, or with
-//     PB_SWAP_IN=zc one zero-copy kernel per layer reading the mapped pinned tier;
+//     step's swap-ins and attention do not queue behind it (pb_tier_set_policy can put it on
+//     the copy stream, or run it concurrently with the swap-ins);
+//   * swap-in is a batched H2D into staging plus a scatter kernel per layer block, or (policy
+//     PB_SWAP_IN_ZERO_COPY) one zero-copy kernel per layer reading the mapped pinned tier;
 //   * the swap-out GATHER (device pages -> contiguous staging) runs first, on the compute
 //     stream, so device slots vacated by swap-out can be refilled in the same step by restore /
 //     rematerialize / append (the reference reuses them LIFO, src/paged_kv_cache.cpp:28-37)
 //     without a read-after-write hazard; the swap-in scatter waits for that gather;
 //   * across steps the D2H is decoupled from the copy stream: a step's swap-ins wait for the
-//     previous step's D2H only when they read a host slot it writes, and a D2H waits for the
-//     previous step's swap-ins (a host slot freed by restore may be reused at once).
+//     newest in-flight D2H (of any earlier step) that writes a host slot they read, and a D2H
+//     waits for the previous step's swap-ins (a host slot freed by restore may be reused);
+//   * within a step, a chunk evicted and restored again is restored device-to-device from
+//     the swap-out staging (its host copy is dead and its D2H skipped), and an out-move whose
+//     host slot a later out-move reuses is dropped (include/pensieve_b200.h has the rules).
 // Host tier layout: [host_slot][layer][K|V][page] — one chunk's bytes for all layers are
 // contiguous (= ModelConfig::chunk_bytes per worker, src/model_config.cpp:36-40), so a
 // swap-out is one D2H per chunk; a swap-in reads one (K,V) block per chunk per layer.
@@ -26,8 +29,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <deque>
 #include <memory>
-#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -117,30 +120,12 @@ __global__ void __launch_bounds__(256) swap_scatter_block_kernel(const uint8_t* 
     }
 }
 
-int n_sms() {
-    static int s = 0;
-    if (!s) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
-        if (s <= 0) s = 148;
-    }
-    return s;
-}
+int n_sms() { return device_sms(); }
 
 // Batched copies (one driver call per batch, cudaMemcpyBatchAsync); per-copy fallback if the
 // runtime refuses the batch.
 void copy_batch(std::vector<void*>& dst, std::vector<void*>& src, std::vector<size_t>& sizes, cudaStream_t st) {
     if (dst.empty()) return;
-    static const int use_batch = [] { // profiling knob: 0 = one cudaMemcpyAsync per piece
-        const char* e = std::getenv("PB_SWAP_BATCH");
-        return e ? std::atoi(e) : 1;
-    }();
-    if (!use_batch) {
-        for (size_t i = 0; i < dst.size(); ++i)
-            cuda_check(cudaMemcpyAsync(dst[i], src[i], sizes[i], cudaMemcpyDefault, st), "swap copy");
-        return;
-    }
     cudaMemcpyAttributes attr{};
     attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
     size_t attr_idx = 0, fail_idx = 0;
@@ -169,18 +154,47 @@ struct pb_kv_tier {
     int32_t* h_slots[2] = {};      // pinned staging for the slot lists
     cudaEvent_t done_p[2] = {};    // swap-ins of the step with this parity done (copy stream)
     cudaEvent_t d2h_p[2] = {};     // swap-out D2H of the step with this parity done
-    cudaEvent_t d2h_prev = nullptr; // last issued swap-out D2H (host-slot RAW for swap-ins)
-    std::vector<int32_t> prev_out_dst; // host slots the previous step's D2H writes (sorted)
+    // D2H copies not yet known complete: the host slots each one writes (sorted) and the event
+    // recorded after it.  Every D2H runs on one stream (the tier's own, or the copy stream),
+    // so waiting for the newest entry that writes a slot also covers the older ones.
+    struct InFlight {
+        cudaEvent_t ev;
+        std::vector<int32_t> slots;
+    };
+    std::deque<InFlight> d2h_inflight;
+    std::vector<cudaEvent_t> ev_pool;
     int par = 0;
     const uint8_t* host_dev = nullptr; // device alias of the pinned tier (zero-copy swap-in)
-    cudaStream_t d2h = nullptr;    // duplex mode: swap-out D2H on its own stream
-    int mode_zc = 0, mode_duplex = 0;
+    cudaStream_t d2h = nullptr;    // swap-out D2H stream (PB_D2H_AFTER_SWAP_IN / _CONCURRENT)
+    int swap_in = PB_SWAP_IN_STAGED, d2h_order = PB_D2H_AFTER_SWAP_IN;
     int layer_block = 1;           // staged swap-in: layers per H2D piece (larger pieces, coarser events)
     pb_event_log* log = nullptr;   // optional: stamps SWAP_IN_LAYER / SWAP_OUT
     cudaEvent_t gathered = nullptr, done = nullptr, in_done = nullptr;
     std::vector<cudaEvent_t> layer_ready;
-    bool any_in = false;
     int64_t chunk_bytes() const { return static_cast<int64_t>(n_layer) * 2 * page_bytes; }
+
+    cudaEvent_t take_event() {
+        if (ev_pool.empty()) {
+            cudaEvent_t e = nullptr;
+            cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+            return e;
+        }
+        cudaEvent_t e = ev_pool.back();
+        ev_pool.pop_back();
+        return e;
+    }
+    void retire_completed() { // non-blocking: drop the D2H entries whose event has fired
+        while (!d2h_inflight.empty()) {
+            const cudaError_t q = cudaEventQuery(d2h_inflight.front().ev);
+            if (q == cudaErrorNotReady) {
+                cudaGetLastError(); // not an error: do not leave it for the next launch check
+                break;
+            }
+            if (q != cudaSuccess) cuda_check(q, "swap-out completion query");
+            ev_pool.push_back(d2h_inflight.front().ev);
+            d2h_inflight.pop_front();
+        }
+    }
 };
 
 extern "C" {
@@ -216,22 +230,13 @@ pb_status pb_tier_create(int32_t n_layer, int32_t host_slots, int64_t page_bytes
             cuda_check(cudaEventCreateWithFlags(&T->done_p[b], cudaEventDisableTiming), "event");
             cuda_check(cudaEventCreateWithFlags(&T->d2h_p[b], cudaEventDisableTiming), "event");
         }
-        cuda_check(cudaEventCreateWithFlags(&T->d2h_prev, cudaEventDisableTiming), "event");
         void* hd = nullptr;
         if (cudaHostGetDevicePointer(&hd, T->host, 0) == cudaSuccess) T->host_dev = static_cast<const uint8_t*>(hd);
         else cudaGetLastError();
-        // transfer policy: zero-copy swap-in (default) or staged H2D + scatter; swap-out D2H
-        // behind the swap-ins (reference order, default) or on its own stream (duplex)
-        const char* m = std::getenv("PB_SWAP_IN");
-        T->mode_zc = T->host_dev && m && std::string(m) == "zc"; // staged measured faster
-        const char* dx = std::getenv("PB_SWAP_DUPLEX");
-        // 0: D2H queued behind the swap-ins on the copy stream (the reference's order);
-        // 1: D2H concurrent with the swap-ins on its own stream; 2 (default): on its own stream
-        // after this step's swap-ins, so the swap-ins (on the attention's critical path) get
-        // the link alone and the D2H overlaps the following steps (measured, profiles/)
-        T->mode_duplex = dx ? std::atoi(dx) : 2;
-        const char* lb = std::getenv("PB_SWAP_LB");
-        T->layer_block = std::max(1, std::min(n_layer, lb ? std::atoi(lb) : kDefaultLayerBlock));
+        // default policy (measured, profiles/): staged swap-in in 8-layer pieces; D2H on the
+        // tier's stream after the step's swap-ins, so the swap-ins (on the attention's
+        // critical path) get the link alone and the D2H overlaps the following steps
+        T->layer_block = std::max(1, std::min(n_layer, kDefaultLayerBlock));
         cuda_check(cudaStreamCreateWithFlags(&T->d2h, cudaStreamNonBlocking), "d2h stream");
         cuda_check(cudaEventCreateWithFlags(&T->gathered, cudaEventDisableTiming), "event");
         cuda_check(cudaEventCreateWithFlags(&T->in_done, cudaEventDisableTiming), "event");
@@ -239,6 +244,33 @@ pb_status pb_tier_create(int32_t n_layer, int32_t host_slots, int64_t page_bytes
         T->layer_ready.resize(static_cast<size_t>(n_layer));
         for (auto& e : T->layer_ready) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
         *out = T.release();
+    });
+}
+
+pb_status pb_tier_set_policy(pb_kv_tier* T, int32_t swap_in, int32_t d2h, int32_t layers_per_piece) {
+    return guarded([&] {
+        if (!T) fail(PB_ERR_ERROR, "null tier");
+        if (swap_in != PB_SWAP_IN_STAGED && swap_in != PB_SWAP_IN_ZERO_COPY)
+            fail(PB_ERR_CONFIG, "unknown swap-in method");
+        if (swap_in == PB_SWAP_IN_ZERO_COPY && !T->host_dev)
+            fail(PB_ERR_UNSUPPORTED, "zero-copy swap-in needs a mapped pinned tier");
+        if (d2h != PB_D2H_ON_COPY_STREAM && d2h != PB_D2H_CONCURRENT && d2h != PB_D2H_AFTER_SWAP_IN)
+            fail(PB_ERR_CONFIG, "unknown swap-out ordering");
+        if (layers_per_piece < 0 || layers_per_piece > T->n_layer)
+            fail(PB_ERR_CONFIG, "layers_per_piece must be in [0, n_layer]");
+        // the D2H stream changes: everything issued so far must be done first
+        for (int b = 0; b < 2; ++b) {
+            cuda_check(cudaEventSynchronize(T->done_p[b]), "policy change");
+            cuda_check(cudaEventSynchronize(T->d2h_p[b]), "policy change");
+        }
+        for (auto& f : T->d2h_inflight) {
+            cuda_check(cudaEventSynchronize(f.ev), "policy change");
+            T->ev_pool.push_back(f.ev);
+        }
+        T->d2h_inflight.clear();
+        T->swap_in = swap_in;
+        T->d2h_order = d2h;
+        if (layers_per_piece > 0) T->layer_block = layers_per_piece;
     });
 }
 
@@ -259,7 +291,11 @@ void pb_tier_destroy(pb_kv_tier* T) {
         cudaFree(T->d_slots[b]);
         cudaFreeHost(T->h_slots[b]);
     }
-    if (T->d2h_prev) cudaEventDestroy(T->d2h_prev);
+    for (auto& f : T->d2h_inflight) {
+        cudaEventSynchronize(f.ev);
+        cudaEventDestroy(f.ev);
+    }
+    for (auto e : T->ev_pool) cudaEventDestroy(e);
     cudaFreeHost(T->host);
     if (T->d2h) {
         cudaStreamSynchronize(T->d2h);
@@ -289,11 +325,36 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         for (int64_t i = 0; i < n_in; ++i)
             if (in_moves[i].src_slot < 0 || in_moves[i].src_slot >= T->host_slots || in_moves[i].dst_slot < 0)
                 fail(PB_ERR_ERROR, "swap-in move needs a host source and a device destination slot");
+        // ---- classify the step's moves (evictions precede restores within a step) ----
+        // from_stage[j] = out-move whose staged bytes restore in-move j (same chunk evicted to
+        // the host slot it is restored from, this step), else -1
+        std::vector<int64_t> from_stage(static_cast<size_t>(n_in), -1);
+        std::vector<char> live(static_cast<size_t>(n_out), 1);
+        for (int64_t j = 0; j < n_in; ++j)
+            for (int64_t i = n_out - 1; i >= 0; --i)
+                if (out_moves[i].chunk == in_moves[j].chunk && out_moves[i].dst_slot == in_moves[j].src_slot) {
+                    from_stage[static_cast<size_t>(j)] = i;
+                    live[static_cast<size_t>(i)] = 0; // host copy dead: restore freed the slot
+                    break;
+                }
+        {
+            // a later out-move to the same host slot means the earlier chunk left that slot
+            // (dropped from the host) in between: only the last write is live
+            std::vector<std::pair<int32_t, int64_t>> by_slot;
+            for (int64_t i = 0; i < n_out; ++i) by_slot.push_back({out_moves[i].dst_slot, i});
+            std::sort(by_slot.begin(), by_slot.end());
+            for (size_t a = 0; a + 1 < by_slot.size(); ++a)
+                if (by_slot[a].first == by_slot[a + 1].first) live[static_cast<size_t>(by_slot[a].second)] = 0;
+        }
+        int64_t n_host_in = 0, n_live_out = 0;
+        for (int64_t j = 0; j < n_in; ++j) n_host_in += from_stage[static_cast<size_t>(j)] < 0;
+        for (int64_t i = 0; i < n_out; ++i) n_live_out += live[static_cast<size_t>(i)];
         cudaStream_t cs = as_stream(compute_stream), xs = as_stream(copy_stream);
         // this step's buffers were last used two steps ago: only that step must be done
         const int par = T->par;
         T->par ^= 1;
         cuda_check(cudaEventSynchronize(T->done_p[par]), "swap step ordering");
+        T->retire_completed();
         int32_t* h_slots = T->h_slots[par];
         int32_t* d_slots = T->d_slots[par];
         uint8_t* stage_out = T->stage_out[par];
@@ -303,29 +364,37 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         for (int64_t i = 0; i < n_in; ++i) h_slots[2 * T->max_chunks + i] = in_moves[i].src_slot;
         cuda_check(cudaMemcpyAsync(d_slots, h_slots, sizeof(int32_t) * 3 * T->max_chunks, cudaMemcpyHostToDevice, cs),
                    "slot upload");
-        // host-slot hazards: a swap-in may read a host slot the previous step's swap-out writes
-        // (RAW: then the swap-ins wait for that D2H; older steps' D2H are done, synchronised
-        // above), and restore frees host slots at once, so this step's swap-out may overwrite
-        // a slot one of this step's swap-ins reads (WAR: then the D2H waits for the swap-ins,
-        // the reference's order, src/swap_engine.cpp:50-53)
-        bool raw = false;
-        for (int64_t j = 0; j < n_in && !raw; ++j)
-            raw = std::binary_search(T->prev_out_dst.begin(), T->prev_out_dst.end(), in_moves[j].src_slot);
-        bool war = false;
-        for (int64_t i = 0; i < n_out && !war; ++i)
+        // RAW across steps: a swap-in from the host reads a slot some earlier step's D2H may
+        // still be writing -> wait for the newest such D2H
+        cudaEvent_t raw_ev = nullptr;
+        for (auto it = T->d2h_inflight.rbegin(); it != T->d2h_inflight.rend() && !raw_ev; ++it)
             for (int64_t j = 0; j < n_in; ++j)
-                if (out_moves[i].dst_slot == in_moves[j].src_slot) {
+                if (from_stage[static_cast<size_t>(j)] < 0 &&
+                    std::binary_search(it->slots.begin(), it->slots.end(), in_moves[j].src_slot)) {
+                    raw_ev = it->ev;
+                    break;
+                }
+        // WAR within the step: a live swap-out overwrites a host slot a restore of another
+        // chunk reads (restore frees host slots at once) -> that D2H follows the swap-ins
+        bool war = false;
+        for (int64_t i = 0; i < n_out && !war; ++i) {
+            if (!live[static_cast<size_t>(i)]) continue;
+            for (int64_t j = 0; j < n_in; ++j)
+                if (from_stage[static_cast<size_t>(j)] < 0 && out_moves[i].dst_slot == in_moves[j].src_slot) {
                     war = true;
                     break;
                 }
+        }
         const int64_t pb = T->page_bytes;
         auto* kp = static_cast<uint8_t*>(k_pool);
         auto* vp = static_cast<uint8_t*>(v_pool);
         // 1. swap-out gather on the compute stream, before any same-step write to those slots;
-        // stage_out[par] is free once the D2H of two steps ago is done (a stream wait, so the
-        // host does not block on a D2H that may still run under later steps' attention)
+        // stage_out[par] is free once the D2H of two steps ago is done, and the device slots it
+        // reads may have been filled by the previous step's swap-ins (stream waits: the host
+        // never blocks on a D2H that may still run under later steps' attention)
         if (n_out > 0) {
             cuda_check(cudaStreamWaitEvent(cs, T->d2h_p[par], 0), "stream wait");
+            cuda_check(cudaStreamWaitEvent(cs, T->done_p[par ^ 1], 0), "stream wait");
             const int64_t jobs = n_out * T->n_layer * 2;
             const int grid = static_cast<int>(std::min<int64_t>(jobs, n_sms() * 8));
             swap_gather_kernel<<<grid, 256, 0, cs>>>(kp, vp, layer_stride, pb, d_slots, static_cast<int32_t>(n_out),
@@ -335,13 +404,14 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
         }
         cuda_check(cudaEventRecord(T->gathered, cs), "event record");
         cuda_check(cudaStreamWaitEvent(xs, T->gathered, 0), "stream wait");
-        if (raw) cuda_check(cudaStreamWaitEvent(xs, T->d2h_prev, 0), "stream wait");
-        // 2. swap-in, layer by layer: H2D (batched) into staging, scatter, per-layer event
-        T->any_in = n_in > 0;
+        if (raw_ev) cuda_check(cudaStreamWaitEvent(xs, raw_ev, 0), "stream wait");
+        // 2. swap-in, layer by layer: H2D (batched) into staging, scatter, per-layer event;
+        // chunks restored from this step's own swap-out come device-to-device from stage_out
+        const bool zc = T->swap_in == PB_SWAP_IN_ZERO_COPY && n_host_in == n_in;
         std::vector<void*> dst, src;
         std::vector<size_t> sz;
         for (int32_t l = 0; l < T->n_layer; ++l) {
-            if (n_in > 0 && T->mode_zc) {
+            if (n_in > 0 && zc) {
                 const int64_t vecs = n_in * 2 * (pb / 16);
                 const int grid = static_cast<int>(std::max<int64_t>(1, std::min<int64_t>((vecs + 1023) / 1024, n_sms() * 4)));
                 swap_in_zc_layer_kernel<<<grid, 256, 0, xs>>>(T->host_dev, T->chunk_bytes(), static_cast<int64_t>(l) * 2 * pb,
@@ -358,13 +428,22 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
                 src.clear();
                 sz.clear();
                 uint8_t* stage_b = stage_in + static_cast<int64_t>(l) * n_in * 2 * pb;
+                const int64_t layer_off = static_cast<int64_t>(l) * 2 * pb;
                 for (int64_t i = 0; i < n_in; ++i) {
+                    const int64_t o = from_stage[static_cast<size_t>(i)];
+                    if (o >= 0) continue;
                     dst.push_back(stage_b + i * nl * 2 * pb);
-                    src.push_back(T->host + static_cast<int64_t>(in_moves[i].src_slot) * T->chunk_bytes() +
-                                  static_cast<int64_t>(l) * 2 * pb);
+                    src.push_back(T->host + static_cast<int64_t>(in_moves[i].src_slot) * T->chunk_bytes() + layer_off);
                     sz.push_back(static_cast<size_t>(nl * 2 * pb));
                 }
                 copy_batch(dst, src, sz, xs);
+                for (int64_t i = 0; i < n_in; ++i) {
+                    const int64_t o = from_stage[static_cast<size_t>(i)];
+                    if (o < 0) continue;
+                    cuda_check(cudaMemcpyAsync(stage_b + i * nl * 2 * pb, stage_out + o * T->chunk_bytes() + layer_off,
+                                               static_cast<size_t>(nl * 2 * pb), cudaMemcpyDeviceToDevice, xs),
+                               "swap-in from staging");
+                }
                 const int grid = static_cast<int>(std::min<int64_t>(n_in * nl * 2, n_sms() * 4));
                 swap_scatter_block_kernel<<<grid, 256, 0, xs>>>(stage_b, kp, vp, layer_stride, l, nl, pb,
                                                                d_slots + T->max_chunks, static_cast<int32_t>(n_in));
@@ -377,13 +456,13 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
             }
             cuda_check(cudaEventRecord(T->layer_ready[static_cast<size_t>(l)], xs), "event record");
         }
-        // 3. swap-out D2H: behind the swap-ins on the copy stream (the reference's order, no
-        // duplex contention on the link), or concurrently on its own stream (duplex mode)
+        // 3. swap-out D2H of the live out-moves.  Every D2H of the tier runs on one stream (the
+        // tier's own, or the copy stream for PB_D2H_ON_COPY_STREAM) so they complete in order.
         cudaStream_t os = xs;
-        if (T->mode_duplex && !war) {
+        if (T->d2h_order != PB_D2H_ON_COPY_STREAM) {
             os = T->d2h;
             cuda_check(cudaStreamWaitEvent(os, T->gathered, 0), "stream wait");
-            if (T->mode_duplex == 2 && n_in > 0) {
+            if (n_in > 0 && (T->d2h_order == PB_D2H_AFTER_SWAP_IN || war)) {
                 cuda_check(cudaEventRecord(T->in_done, xs), "event record");
                 cuda_check(cudaStreamWaitEvent(os, T->in_done, 0), "stream wait");
             }
@@ -391,30 +470,29 @@ pb_status pb_swap_step(pb_kv_tier* T, void* k_pool, void* v_pool, int64_t layer_
             // D2H reuses (restore frees host slots at once)
             cuda_check(cudaStreamWaitEvent(os, T->done_p[par ^ 1], 0), "stream wait");
         }
-        if (n_out > 0) {
+        if (n_live_out > 0) {
             dst.clear();
             src.clear();
             sz.clear();
+            std::vector<int32_t> slots;
             for (int64_t i = 0; i < n_out; ++i) {
+                if (!live[static_cast<size_t>(i)]) continue;
                 dst.push_back(T->host + static_cast<int64_t>(out_moves[i].dst_slot) * T->chunk_bytes());
                 src.push_back(stage_out + i * T->chunk_bytes());
                 sz.push_back(static_cast<size_t>(T->chunk_bytes()));
+                slots.push_back(out_moves[i].dst_slot);
             }
             copy_batch(dst, src, sz, os);
             if (T->log) {
                 const pb_status r = pb_evlog_mark(T->log, PB_EV_SWAP_OUT, -1, -1, os);
                 if (r != PB_OK) fail(r, "swap-out stamp");
             }
+            std::sort(slots.begin(), slots.end());
+            cudaEvent_t e = T->take_event();
+            cuda_check(cudaEventRecord(e, os), "event record");
+            T->d2h_inflight.push_back({e, std::move(slots)});
         }
-        // the D2H no longer joins the copy stream: the next step's swap-ins only wait for it
-        // on a real RAW hazard
         cuda_check(cudaEventRecord(T->d2h_p[par], os), "event record");
-        T->prev_out_dst.clear();
-        if (n_out > 0) {
-            cuda_check(cudaEventRecord(T->d2h_prev, os), "event record");
-            for (int64_t i = 0; i < n_out; ++i) T->prev_out_dst.push_back(out_moves[i].dst_slot);
-            std::sort(T->prev_out_dst.begin(), T->prev_out_dst.end());
-        }
         cuda_check(cudaEventRecord(T->done_p[par], xs), "event record");
         cuda_check(cudaEventRecord(T->done, xs), "event record");
     });
@@ -440,6 +518,8 @@ pb_status pb_swap_sync(pb_kv_tier* T) {
         if (!T) fail(PB_ERR_ERROR, "null tier");
         cuda_check(cudaEventSynchronize(T->done), "swap sync");
         for (int b = 0; b < 2; ++b) cuda_check(cudaEventSynchronize(T->d2h_p[b]), "swap sync");
+        for (auto& f : T->d2h_inflight) cuda_check(cudaEventSynchronize(f.ev), "swap sync");
+        T->retire_completed();
     });
 }
 

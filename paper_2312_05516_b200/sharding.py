@@ -11,23 +11,20 @@ from __future__ import annotations
 
 import numpy as np
 
-from .abi import AttnShape, Batch, DimensionMismatch
+from . import abi
+from .abi import AttnShape, Batch
 
 
 def shard_shape(shape: AttnShape, rank: int, world: int) -> AttnShape:
-    if world < 1 or not 0 <= rank < world:
-        raise ValueError("bad rank/world")
-    if shape.n_kv_head % world:
-        raise DimensionMismatch(f"n_kv_head {shape.n_kv_head} not divisible by {world} partitions")
-    nkv = shape.n_kv_head // world
-    nh = shape.n_head // world
-    return AttnShape(nh, nkv, shape.head_size, shape.chunk_size, shape.n_slots, shape.dtype, shape.scale)
+    """The rank's shard shape (pb_shard_shape; ConfigError for a bad rank, DimensionMismatch
+    when n_kv_head % world != 0)."""
+    return abi.shard_shape(shape, rank, world)[0]
 
 
 def shard_heads(shape: AttnShape, rank: int, world: int):
     """(first query head, first kv head) of the rank's shard."""
-    s = shard_shape(shape, rank, world)
-    return rank * s.n_head, rank * s.n_kv_head
+    _, h0, k0 = abi.shard_shape(shape, rank, world)
+    return h0, k0
 
 
 def pack_batch(b: Batch) -> np.ndarray:

@@ -6,7 +6,12 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-from paper_2312_05516_b200.abi import KvCache, KvTier  # noqa: E402
+from paper_2312_05516_b200.abi import (PB_D2H_AFTER_SWAP_IN, PB_D2H_CONCURRENT,  # noqa: E402
+                                       PB_D2H_ON_COPY_STREAM, PB_SWAP_IN_STAGED, PB_SWAP_IN_ZERO_COPY,
+                                       KvCache, KvTier)
+
+D2H_MODES = [PB_D2H_AFTER_SWAP_IN, PB_D2H_CONCURRENT, PB_D2H_ON_COPY_STREAM]
+SWAP_IN = [PB_SWAP_IN_STAGED, PB_SWAP_IN_ZERO_COPY]
 
 
 def _pools(torch, n_layer, n_slots, page_bytes, seed):
@@ -42,18 +47,17 @@ def test_swap_out_then_in_roundtrip(cuda):
             assert np.array_equal(kn[l, dd], k0[l, d]) and np.array_equal(vn[l, dd], v0[l, d])
 
 
-@pytest.mark.parametrize("d2h_mode", ["2", "1", "0"])  # D2H after / concurrent with / behind swap-ins
-@pytest.mark.parametrize("swap_in", ["staged", "zc"])
-def test_same_step_slot_reuse_hazard(cuda, monkeypatch, d2h_mode, swap_in):
+@pytest.mark.parametrize("d2h_mode", D2H_MODES)  # D2H after / concurrent with / behind swap-ins
+@pytest.mark.parametrize("swap_in", SWAP_IN)
+def test_same_step_slot_reuse_hazard(cuda, d2h_mode, swap_in):
     """A device slot vacated by swap-out is refilled by a swap-in in the SAME step (the LIFO
     reclaim makes this common): the host must get the old bytes, the device the new ones."""
-    monkeypatch.setenv("PB_SWAP_DUPLEX", d2h_mode)  # read when the tier is created
-    monkeypatch.setenv("PB_SWAP_IN", swap_in)
     torch = cuda
     L, n_slots, page = 4, 8, 4096
     k, v = _pools(torch, L, n_slots, page, 2)
     k0, v0 = k.cpu().numpy().copy(), v.cpu().numpy().copy()
     tier = KvTier(L, 4, page, 4)
+    tier.set_policy(swap_in, d2h_mode)
     host = tier.host_view().reshape(4, L, 2, page)
     rng = np.random.default_rng(3)
     host[2] = rng.integers(0, 256, size=(L, 2, page), dtype=np.uint8)  # chunk resident on host slot 2
@@ -99,20 +103,19 @@ def test_cache_moves_drive_the_engine(cuda):
         assert np.array_equal(kn[:, s], truth[c][0]) and np.array_equal(vn[:, s], truth[c][1])
 
 
-@pytest.mark.parametrize("d2h_mode", ["2", "1", "0"])  # D2H after / concurrent with / behind swap-ins
-@pytest.mark.parametrize("swap_in", ["staged", "zc"])
-def test_host_slot_hazards_across_and_within_steps(cuda, monkeypatch, d2h_mode, swap_in):
+@pytest.mark.parametrize("d2h_mode", D2H_MODES)  # D2H after / concurrent with / behind swap-ins
+@pytest.mark.parametrize("swap_in", SWAP_IN)
+def test_host_slot_hazards_across_and_within_steps(cuda, d2h_mode, swap_in):
     """Host-side hazards of the double-buffered engine: (a) a swap-in in step s+1 from the host
     slot step s swapped out to (RAW across steps, without a host sync in between) gets the
     swapped-out bytes; (b) in one step, a swap-in reading host slot X and a swap-out writing X
     (restore frees X at once, src/paged_kv_cache.cpp:190) -- the swap-in gets the OLD bytes."""
-    monkeypatch.setenv("PB_SWAP_DUPLEX", d2h_mode)  # read when the tier is created
-    monkeypatch.setenv("PB_SWAP_IN", swap_in)
     torch = cuda
     L, n_slots, page = 6, 16, 8192
     k, v = _pools(torch, L, n_slots, page, 4)
     k0, v0 = k.cpu().numpy().copy(), v.cpu().numpy().copy()
     tier = KvTier(L, 6, page, 4)
+    tier.set_policy(swap_in, d2h_mode)
     host = tier.host_view().reshape(6, L, 2, page)
     rng = np.random.default_rng(5)
     host[3] = rng.integers(0, 256, size=(L, 2, page), dtype=np.uint8)
@@ -136,20 +139,19 @@ def test_host_slot_hazards_across_and_within_steps(cuda, monkeypatch, d2h_mode, 
         assert np.array_equal(host[3, l, 0], k0[l, 4]) and np.array_equal(host[3, l, 1], v0[l, 4])
 
 
-@pytest.mark.parametrize("d2h_mode", ["2", "1", "0"])  # D2H after / concurrent with / behind swap-ins
-@pytest.mark.parametrize("swap_in", ["staged", "zc"])
-def test_cross_step_war_on_a_freed_host_slot(cuda, monkeypatch, d2h_mode, swap_in):
+@pytest.mark.parametrize("d2h_mode", D2H_MODES)  # D2H after / concurrent with / behind swap-ins
+@pytest.mark.parametrize("swap_in", SWAP_IN)
+def test_cross_step_war_on_a_freed_host_slot(cuda, d2h_mode, swap_in):
     """The D2H no longer joins the copy stream, so a step's swap-out could race the previous
     step's swap-in from the same host slot (restore frees it at once and the next eviction may
     reuse it).  Step 1 swaps host slot 5 in; step 2, issued right away with no layer wait on the
     compute stream, swaps a device slot out to host slot 5: step 1 must still read the OLD bytes."""
-    monkeypatch.setenv("PB_SWAP_DUPLEX", d2h_mode)  # read when the tier is created
-    monkeypatch.setenv("PB_SWAP_IN", swap_in)
     torch = cuda
     L, n_slots, page = 8, 16, 1 << 16
     k, v = _pools(torch, L, n_slots, page, 6)
     k0, v0 = k.cpu().numpy().copy(), v.cpu().numpy().copy()
     tier = KvTier(L, 8, page, 8)
+    tier.set_policy(swap_in, d2h_mode)
     host = tier.host_view().reshape(8, L, 2, page)
     rng = np.random.default_rng(7)
     host[:] = rng.integers(0, 256, size=host.shape, dtype=np.uint8)
@@ -168,3 +170,84 @@ def test_cross_step_war_on_a_freed_host_slot(cuda, monkeypatch, d2h_mode, swap_i
         for h in range(8):
             assert np.array_equal(kn[l, 8 + h], old[h, l, 0]) and np.array_equal(vn[l, 8 + h], old[h, l, 1])
         assert np.array_equal(host[5, l, 0], k0[l, 1]) and np.array_equal(host[5, l, 1], v0[l, 1])
+
+
+@pytest.mark.parametrize("d2h_mode", D2H_MODES)
+@pytest.mark.parametrize("swap_in", SWAP_IN)
+def test_evict_then_restore_same_chunk_in_one_step(cuda, d2h_mode, swap_in):
+    """make_room can evict a queued conversation's chunk (device d -> host h) and a later
+    admission in the SAME step restore it (host h -> device d').  The restore must get the
+    evicted bytes (from the swap-out staging), not the stale host slot; the dead host copy is
+    not written, so a later eviction into h in the same step owns it."""
+    torch = cuda
+    L, n_slots, page = 5, 16, 4096
+    k, v = _pools(torch, L, n_slots, page, 8)
+    k0, v0 = k.cpu().numpy().copy(), v.cpu().numpy().copy()
+    tier = KvTier(L, 4, page, 4)
+    tier.set_policy(swap_in, d2h_mode)
+    host = tier.host_view().reshape(4, L, 2, page)
+    host[:] = 7  # stale bytes
+    cs, xs = torch.cuda.Stream(), torch.cuda.Stream()
+    # chunk 5: device 3 -> host 1 -> device 12; then chunk 6: device 4 -> host 1 (slot reused)
+    tier.step(k.data_ptr(), v.data_ptr(), n_slots * page, [(5, 3, 1), (6, 4, 1)], [(5, 1, 12)],
+              cs.cuda_stream, xs.cuda_stream)
+    for l in range(L):
+        tier.wait_layer(l, cs.cuda_stream)
+    tier.sync()
+    torch.cuda.synchronize()
+    kn, vn = k.cpu().numpy(), v.cpu().numpy()
+    for l in range(L):
+        assert np.array_equal(kn[l, 12], k0[l, 3]) and np.array_equal(vn[l, 12], v0[l, 3])
+        assert np.array_equal(host[1, l, 0], k0[l, 4]) and np.array_equal(host[1, l, 1], v0[l, 4])
+
+
+@pytest.mark.parametrize("d2h_mode", [PB_D2H_AFTER_SWAP_IN, PB_D2H_CONCURRENT])
+@pytest.mark.parametrize("swap_in", SWAP_IN)
+def test_raw_two_steps_back(cuda, d2h_mode, swap_in):
+    """Step 1 swaps out to host slot h, step 2 moves nothing, step 3 restores from h with no
+    swap-outs: the restore must wait for step 1's D2H (still in flight on the D2H stream),
+    not only for the previous step's."""
+    torch = cuda
+    L, n_slots, page = 8, 16, 1 << 17  # 2 MiB per chunk: the D2H is still running at step 3
+    k, v = _pools(torch, L, n_slots, page, 9)
+    k0, v0 = k.cpu().numpy().copy(), v.cpu().numpy().copy()
+    tier = KvTier(L, 4, page, 4)
+    tier.set_policy(swap_in, d2h_mode)
+    host = tier.host_view().reshape(4, L, 2, page)
+    host[:] = 3
+    cs, xs = torch.cuda.Stream(), torch.cuda.Stream()
+    stride = n_slots * page
+    tier.step(k.data_ptr(), v.data_ptr(), stride, [(1, 2, 0), (2, 5, 3)], [], cs.cuda_stream, xs.cuda_stream)
+    tier.step(k.data_ptr(), v.data_ptr(), stride, [], [], cs.cuda_stream, xs.cuda_stream)
+    tier.step(k.data_ptr(), v.data_ptr(), stride, [], [(1, 0, 9), (2, 3, 10)], cs.cuda_stream, xs.cuda_stream)
+    for l in range(L):
+        tier.wait_layer(l, cs.cuda_stream)
+    tier.sync()
+    torch.cuda.synchronize()
+    kn, vn = k.cpu().numpy(), v.cpu().numpy()
+    for l in range(L):
+        assert np.array_equal(kn[l, 9], k0[l, 2]) and np.array_equal(vn[l, 9], v0[l, 2])
+        assert np.array_equal(kn[l, 10], k0[l, 5]) and np.array_equal(vn[l, 10], v0[l, 5])
+
+
+def test_policy_validation(cuda):
+    from paper_2312_05516_b200.abi import ConfigError
+    tier = KvTier(2, 2, 256, 2)
+    with pytest.raises(ConfigError):
+        tier.set_policy(5, PB_D2H_AFTER_SWAP_IN)
+    with pytest.raises(ConfigError):
+        tier.set_policy(PB_SWAP_IN_STAGED, 9)
+    with pytest.raises(ConfigError):
+        tier.set_policy(PB_SWAP_IN_STAGED, PB_D2H_AFTER_SWAP_IN, 3)
+
+
+@pytest.mark.parametrize("world", [1, 2, 4, 8])
+def test_tier_chunk_bytes_is_model_chunk_bytes(cuda, world):
+    """A rank's tier over its shard pages holds ModelConfig::chunk_bytes per chunk
+    (/root/reference/proj/src/model_config.cpp:36-40, n_partitions = world)."""
+    from paper_2312_05516_b200.abi import chunk_bytes, model_preset
+    m = model_preset("llama2-70b")
+    m.n_partitions = world
+    page = 16 * (m.n_kv_head // world) * m.head_size * m.bytes_per_scalar
+    tier = KvTier(m.n_layer, 1, page, 1)
+    assert tier.chunk_bytes == chunk_bytes(m, 16)
