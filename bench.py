@@ -13,7 +13,13 @@ collective on the attention path): total work is fixed, so scaling is "strong".
 
 Prints one JSON line (rank 0).  Timing: CUDA events on the launching stream, barrier +
 synchronize on both sides, max over ranks.  Per-step inputs (n_layer x pool bytes) are far
-larger than the 126 MB L2, so no explicit flush is needed.
+larger than the 126 MB L2, so no explicit flush is needed.  At one GPU the default line also
+carries `configs`: the HBM-bound configs 2 and 3 and the swap config 5 (driven over the
+reference's own ShareGPT trace), each with its roofline fraction and clock record.
+
+Both arms print the same `metric`, `unit` and `config` for a config, so the driver can divide
+them; the reference arm loads only oracle/_ref/libkvsim_ref.so (the workload generators it
+shares with this arm are host-only and never load the product library).
 """
 from __future__ import annotations
 
@@ -32,6 +38,19 @@ sys.path.insert(0, ROOT)
 
 MODEL_LAYERS = {1: 1, 2: 40, 3: 40, 4: 80}
 UNITS = {1: "GB/s", 2: "GB/s", 3: "GB/s", 4: "TFLOP/s"}
+# one metric name per config, printed identically by both arms (BASELINE.json metric:
+# "ragged paged-attn TFLOP/s & HBM GB/s vs roofline; KV swap GB/s; x CPU ref")
+METRICS = {1: "ragged paged-attn HBM GB/s", 2: "ragged paged-attn HBM GB/s", 3: "ragged paged-attn HBM GB/s",
+           4: "ragged paged-attn TFLOP/s"}
+
+
+def bench_config(w, n_layer, world):
+    """The `config` object of a config's line (identical in both arms)."""
+    return {"workload": w.name, "n_layer": n_layer, "spans": len(w.spans), "tokens": w.total_tokens,
+            "n_head": w.n_head, "n_kv_head": w.n_kv_head, "head_size": w.head_size, "page_tokens": w.chunk,
+            "parallelism": f"kv-head shard x{world}", "l2": "inputs larger than L2 (per step: n_layer pools)"}
+
+
 FALLBACK_PEAKS = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 
 
@@ -151,56 +170,60 @@ def metric_value(unit, flops, bytes_, seconds):
 
 
 def bench_reference(args):
+    """The reference's own CPU implementation (oracle/_ref: kvsim::paged_multi_token_attention
+    compiled from /root/reference sources), on all host threads, on this config's workload.
+    A step is one bounded sample of the workload's spans (about --cpu-budget seconds)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return 0
     from paper_2312_05516_b200.workloads import config
     w = config(args.config)
     unit = UNITS[args.config]
+    n_layer = args.layers or MODEL_LAYERS[args.config]
     threads = os.cpu_count() or 1
-    vals = []
+    vals, secs = [], []
     ids = None
     for s in range(args.warmup + args.steps):
         sec, fl, by, ids = run_reference_cpu(w, threads, args.cpu_budget)
         if s >= args.warmup:
             vals.append(metric_value(unit, fl, by, sec))
+            secs.append(sec)
     v = statistics.median(vals)
+    sample = f"{len(ids)} of {len(w.spans)} spans (one layer, all heads), per-span std::thread split"
     line = {
-        "impl": "reference", "metric": f"ragged paged-attn {unit} (reference CPU kvsim::paged_multi_token_attention)",
+        "impl": "reference", "metric": METRICS[args.config],
         "value": v, "unit": unit, "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-        "higher_is_better": True, "dtype": "f32 (bf16-rounded inputs, double accumulation)",
+        "ms_per_step": statistics.median(secs) * 1e3, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32 (bf16-rounded inputs, double accumulation)",
         "data": "synthetic (SplitMix64, workloads.config)",
-        "config": {"workload": w.name, "sample_spans": len(ids)},
-        "cpu_baseline": {"value": v, "unit": unit, "cores": threads, "kind": "reference",
-                         "sample": f"{len(ids)} of {len(w.spans)} spans (one layer), per-span std::thread split"},
+        "config": bench_config(w, n_layer, 1),
+        "cpu_baseline": {"value": v, "unit": unit, "cores": threads, "kind": "reference", "sample": sample},
         "e2e": {"value": v, "unit": unit, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
     return 0
 
 
-def bench_ours(args):
+def measure_attention(args, cfg, n_layer, steps, warmup, rank, world, dev, with_e2e):
+    """One config's attention step on this rank's kv-head shard: device-timed value, per-launch
+    roofline of the dominant kernel (one layer's fused launch), and (with_e2e) the same metric
+    through the C-ABI with host q/out buffers.  Returns a dict (rank 0 reports it)."""
     import torch
     import torch.distributed as dist
 
     from paper_2312_05516_b200 import abi
     from paper_2312_05516_b200.abi import PB_BF16, AttentionPlan
+    from paper_2312_05516_b200.sharding import broadcast_batch, shard_shape
     from paper_2312_05516_b200.workloads import config
 
-    rank, world, local = dist_env()
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
-    w = config(args.config)
-    n_layer = args.layers or MODEL_LAYERS[args.config]
-    unit = UNITS[args.config]
+    w = config(cfg)
+    unit = UNITS[cfg]
     if w.n_kv_head % world:
         raise SystemExit(f"n_kv_head {w.n_kv_head} not divisible by {world} ranks")
     nkv = w.n_kv_head // world
     # every rank gets rank 0's span/block-table descriptors (the same migration plan,
     # PAPER.md:741-744) and its own kv-head shard; no collective touches the attention
-    from paper_2312_05516_b200.sharding import broadcast_batch, shard_shape
     shape = shard_shape(w.shape(), rank, world)
     batch = broadcast_batch(w.batch() if rank == 0 else None) if world > 1 else w.batch()
     dt = torch.bfloat16 if w.dtype == PB_BF16 else torch.float32
@@ -222,7 +245,7 @@ def bench_ours(args):
     out = torch.empty_like(q)
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
-    plan = AttentionPlan(shape, batch, args.plan_flags)
+    plan = AttentionPlan(shape, batch)
     plan.upload(sh)
     ws = torch.zeros(max(1, plan.workspace_bytes()), dtype=torch.uint8, device=dev)
     stats = plan.stats()
@@ -237,19 +260,19 @@ def bench_ours(args):
             dist.barrier()
         torch.cuda.synchronize()
 
-    for _ in range(max(3, args.warmup)):
+    for _ in range(warmup):
         step()
     barrier()
     # ---- timed region: K steps, per-layer events for the dominant kernel's duration ----
-    clocks = ClockSampler(local)
+    clocks = ClockSampler(dev.index)
     clocks.start()
-    n_ev = args.steps * n_layer
+    n_ev = steps * n_layer
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev + 1)]
     launches0 = abi.launch_count()
     barrier()
     ev[0].record(stream)
     i = 0
-    for _ in range(args.steps):
+    for _ in range(steps):
         for l in range(n_layer):
             plan.run(q.data_ptr(), pools_k[l].data_ptr(), pools_v[l].data_ptr(), out.data_ptr(),
                      ws.data_ptr(), sh)
@@ -263,118 +286,214 @@ def bench_ours(args):
     t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_per_step = float(t.item()) / args.steps
-
-    # ---- e2e through the C-ABI with host buffers: plan build+upload, per-layer H2D q and
-    # D2H out from pinned memory, every step ----
-    q_host = torch.empty(q_elems, dtype=dt, pin_memory=True)
-    q_host.copy_(q.cpu())
-    out_host = torch.empty(q_elems, dtype=dt, pin_memory=True)
-    e2e_steps = max(2, min(args.steps, 10))
-    # pb_attn_run_layers_host: every layer's q goes host->device and its output device->host
-    # (pinned buffers), overlapped with the neighbouring layers' attention on two copy streams
-    stage = torch.empty(max(1, plan.stage_bytes()), dtype=torch.uint8, device=dev)
-    kp = [t.data_ptr() for t in pools_k]
-    vp = [t.data_ptr() for t in pools_v]
-    barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    t0 = time.perf_counter()
-    e0.record(stream)
-    for _ in range(e2e_steps):
-        p2 = AttentionPlan(shape, batch, args.plan_flags)
-        p2.upload(sh)
-        p2.run_layers_host([q_host.data_ptr()] * n_layer, [out_host.data_ptr()] * n_layer, kp, vp,
-                           stage.data_ptr(), ws.data_ptr(), sh)
-        stream.synchronize()
-    e1.record(stream)
-    barrier()
-    wall = time.perf_counter() - t0
-    te = torch.tensor([wall], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(te, op=dist.ReduceOp.MAX)
-    e2e_s = float(te.item()) / e2e_steps
-    desc_bytes = 32 * batch.n_spans + 4 * int(batch.bt_off[-1]) + 40 * (stats["prefill_tiles"] + stats["decode_units"] + stats["simt_tiles"])
-
-    if rank != 0:
-        if world > 1:
-            dist.destroy_process_group()
-        return 0
-
-    # whole-job work: every rank computes its kv-head shard of every layer
+    ms_per_step = float(t.item()) / steps
     fl_layer, by_layer = w.flops_bytes()
-    value = metric_value(unit, fl_layer * n_layer, by_layer * n_layer, ms_per_step / 1e3)
-    e2e_value = metric_value(unit, fl_layer * n_layer, by_layer * n_layer, e2e_s)
+    res = {"w": w, "unit": unit, "n_layer": n_layer, "ms_per_step": ms_per_step, "clocks": clk,
+           "gpu_launches": int(launches), "stats": stats,
+           # whole-job work: every rank computes its kv-head shard of every layer
+           "value": metric_value(unit, fl_layer * n_layer, by_layer * n_layer, ms_per_step / 1e3)}
     peaks, peak_src = load_peaks()
-    # dominant kernel: one layer's attention launch on rank 0 (its shard)
     avg_launch_s = statistics.mean(per_launch) / 1e3
     if unit == "TFLOP/s":
         achieved = stats["flops"] / avg_launch_s / 1e12
         peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
-        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s"}
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "peak_kind": "bf16 sustained (kernel timed inside a long step)"}
     else:
         achieved = stats["bytes"] / avg_launch_s / 1e9
         peak = peaks["hbm_gbs"]
-        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s"}
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "peak_kind": "HBM copy"}
     roof["frac"] = achieved / peak
     roof["traffic"] = load_traffic(w.name)
     roof["peak_source"] = peak_src
     roof["per_launch_us"] = avg_launch_s * 1e6
     roof["hbm_gbs"] = stats["bytes"] / avg_launch_s / 1e9
     roof["tflops"] = stats["flops"] / avg_launch_s / 1e12
+    res["roofline"] = roof
 
+    if with_e2e:
+        # ---- e2e through the C-ABI with host buffers, every step: plan build + upload, then
+        # pb_attn_run_layers_host (per-layer H2D of q and D2H of out from pinned memory,
+        # overlapped with the neighbouring layers' attention on two copy streams) ----
+        q_host = torch.empty(q_elems, dtype=dt, pin_memory=True)
+        q_host.copy_(q.cpu())
+        out_host = torch.empty(q_elems, dtype=dt, pin_memory=True)
+        e2e_steps = max(2, min(steps, 10))
+        stage = torch.empty(max(1, plan.stage_bytes()), dtype=torch.uint8, device=dev)
+        kp = [x.data_ptr() for x in pools_k]
+        vp = [x.data_ptr() for x in pools_v]
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            p2 = AttentionPlan(shape, batch)
+            p2.upload(sh)
+            p2.run_layers_host([q_host.data_ptr()] * n_layer, [out_host.data_ptr()] * n_layer, kp, vp,
+                               stage.data_ptr(), ws.data_ptr(), sh)
+            stream.synchronize()
+        barrier()
+        wall = time.perf_counter() - t0
+        te = torch.tensor([wall], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_s = float(te.item()) / e2e_steps
+        desc_bytes = 32 * batch.n_spans + 4 * int(batch.bt_off[-1]) + 40 * (
+            stats["prefill_tiles"] + stats["decode_units"] + stats["simt_tiles"])
+        io_bytes = n_layer * q_elems * eb
+        # pinned-copy peaks of this box (the e2e line is bound by these: every layer's q and
+        # out cross the host link)
+        h2d_peak, d2h_peak = pinned_copy_peaks(torch, dev, 1 << 28)
+        res["e2e"] = {"value": metric_value(unit, fl_layer * n_layer, by_layer * n_layer, e2e_s), "unit": unit,
+                      "h2d_bytes_per_step": io_bytes + desc_bytes, "d2h_bytes_per_step": io_bytes,
+                      "ms_per_step": e2e_s * 1e3,
+                      "link": {"h2d_gbs": (io_bytes + desc_bytes) / e2e_s / 1e9, "d2h_gbs": io_bytes / e2e_s / 1e9,
+                               "pinned_h2d_peak_gbs": h2d_peak, "pinned_d2h_peak_gbs": d2h_peak,
+                               "h2d_frac": (io_bytes + desc_bytes) / e2e_s / 1e9 / h2d_peak,
+                               "d2h_frac": io_bytes / e2e_s / 1e9 / d2h_peak}}
+        del q_host, out_host, stage
+    del pools_k, pools_v, q, out, ws, plan
+    torch.cuda.empty_cache()
+    return res
+
+
+def pinned_copy_peaks(torch, dev, nbytes):
+    """cudaMemcpyAsync pinned H2D and D2H GB/s on this box (best of 3, CUDA events)."""
+    big = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    hbuf = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    big.copy_(hbuf, non_blocking=True)
+    torch.cuda.synchronize()
+    best = [0.0, 0.0]
+    for _ in range(3):
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        e[0].record(); big.copy_(hbuf, non_blocking=True); e[1].record()
+        e[2].record(); hbuf.copy_(big, non_blocking=True); e[3].record()
+        torch.cuda.synchronize()
+        best[0] = max(best[0], nbytes / (e[0].elapsed_time(e[1]) / 1e3) / 1e9)
+        best[1] = max(best[1], nbytes / (e[2].elapsed_time(e[3]) / 1e3) / 1e9)
+    del big, hbuf
+    return best[0], best[1]
+
+
+def duplex_microbench(torch, dev, nbytes=1 << 28, reps=3):
+    """Isolated PCIe/C2C duplex measurement (the paper reports an 18-20% per-direction drop
+    when H2D and D2H overlap; the reference models 0.20,
+    proj/include/kvsim/swap_engine.hpp:15): H2D alone, D2H alone, then both at once on two
+    streams, each timed with CUDA events on its own stream."""
+    dev_a = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    dev_b = torch.empty(nbytes, dtype=torch.uint8, device=dev)
+    h_a = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    h_b = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+
+    def timed(h2d, d2h):
+        torch.cuda.synchronize()
+        e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        if h2d:
+            e[0].record(s1)
+            with torch.cuda.stream(s1):
+                dev_a.copy_(h_a, non_blocking=True)
+            e[1].record(s1)
+        if d2h:
+            e[2].record(s2)
+            with torch.cuda.stream(s2):
+                h_b.copy_(dev_b, non_blocking=True)
+            e[3].record(s2)
+        torch.cuda.synchronize()
+        g = lambda a, b: nbytes / (e[a].elapsed_time(e[b]) / 1e3) / 1e9  # noqa: E731
+        return (g(0, 1) if h2d else None), (g(2, 3) if d2h else None)
+
+    timed(True, True)
+    h_alone = max(timed(True, False)[0] for _ in range(reps))
+    d_alone = max(timed(False, True)[1] for _ in range(reps))
+    both = [timed(True, True) for _ in range(reps)]
+    h_both = max(b[0] for b in both)
+    d_both = max(b[1] for b in both)
+    del dev_a, dev_b, h_a, h_b
+    return {"bytes_each": nbytes, "h2d_alone_gbs": h_alone, "d2h_alone_gbs": d_alone,
+            "h2d_concurrent_gbs": h_both, "d2h_concurrent_gbs": d_both,
+            "h2d_drop": 1 - h_both / h_alone, "d2h_drop": 1 - d_both / d_alone,
+            "paper_drop": "0.18-0.20 per direction (PAPER.md:760-762)", "reference_model": 0.20}
+
+
+def bench_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    n_layer = args.layers or MODEL_LAYERS[args.config]
+    warmup = max(3, args.warmup)
+    r = measure_attention(args, args.config, n_layer, args.steps, warmup, rank, world, dev, with_e2e=True)
+    # the other BASELINE configs at one GPU, each a sub-result with its own roofline and clocks
+    # (configs 2 and 3 have 40 and 10 kv heads: not the multi-GPU workload)
+    subs = {}
+    if world == 1 and args.config == 4 and not args.no_subconfigs:
+        for c in (2, 3):
+            m = measure_attention(args, c, MODEL_LAYERS[c], args.steps, warmup, rank, world, dev, with_e2e=False)
+            subs[f"cfg{c}"] = {"metric": METRICS[c], "value": m["value"], "unit": m["unit"],
+                               "ms_per_step": m["ms_per_step"], "n_layer": m["n_layer"], "workload": m["w"].name,
+                               "roofline": m["roofline"], "clocks": m["clocks"], "gpu_launches": m["gpu_launches"]}
+        subs["cfg5"] = config5_result(args, warmup)
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+    w = r["w"]
+    unit = r["unit"]
     cpu = None
     if not args.no_cpu_baseline:
         threads = os.cpu_count() or 1
         sec, fl, by, ids = run_reference_cpu(w, threads, args.cpu_budget)
         cpu = {"value": metric_value(unit, fl, by, sec), "unit": unit, "cores": threads, "kind": "reference",
-               "sample": f"{len(ids)} of {len(w.spans)} spans, one layer, all {shape.n_head * world} heads; "
+               "sample": f"{len(ids)} of {len(w.spans)} spans, one layer, all {w.n_head} heads; "
                          f"{sec:.2f} s wall on {threads} threads"}
+    cfgd = bench_config(w, n_layer, world)
     line = {
-        "metric": f"ragged paged-attn {unit} (fused prefill+decode, {n_layer} layers/step)",
-        "value": value, "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": max(3, args.warmup),
-        "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "bf16" if w.dtype == PB_BF16 else "f32",
+        "metric": METRICS[args.config],
+        "value": r["value"], "unit": unit, "n_gpus": world, "steps": args.steps, "warmup": warmup,
+        "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16" if w.dtype == 1 else "f32",
         "data": "synthetic (SplitMix64 fill on device; random-init KV pools per layer)",
-        "config": {"workload": w.name, "n_layer": n_layer, "spans": len(w.spans), "tokens": w.total_tokens,
-                   "n_head": w.n_head, "n_kv_head": w.n_kv_head, "head_size": w.head_size, "page_tokens": w.chunk,
-                   "parallelism": f"kv-head shard x{world}",
-                   "l2": "inputs larger than L2 (per step: n_layer pools)",
-                   "plan": {k: stats[k] for k in ("prefill_tiles", "decode_units", "split_spans", "simt_tiles")}},
-        "roofline": roof,
+        "config": cfgd,
+        "roofline": r["roofline"],
+        "plan": {k: r["stats"][k] for k in ("prefill_tiles", "decode_units", "split_spans", "simt_tiles")},
         "cpu_baseline": cpu,
-        "e2e": {"value": e2e_value, "unit": unit,
-                "h2d_bytes_per_step": n_layer * q_elems * eb + desc_bytes,
-                "d2h_bytes_per_step": n_layer * q_elems * eb},
-        "gpu_launches": int(launches),
-        "clocks": clk,
+        "e2e": r["e2e"],
+        "gpu_launches": r["gpu_launches"],
+        "clocks": r["clocks"],
     }
+    if subs:
+        line["configs"] = subs
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
     return 0
 
 
-def plan_sharegpt_steps(n_conv: int, n_steps: int, host_factor: float = 0.5, think: float = 1.0):
-    """Config 5: drive the step planner (pb_sched_*) over a synthetic ShareGPT-like trace with
-    the device tier at ~30% of the working set and a host tier small enough to
-    overflow (so leading chunks get dropped and come back as recompute spans); return the
-    planned steps (ragged batch + swap slot moves) starting at the first step that carries a
-    dropped-prefix recompute span (or, failing that, the first swap-in)."""
+def plan_sharegpt_steps(n_steps: int, dev_frac: float = 0.3, host_factor: float = 0.05, think: float = 1.0):
+    """Config 5: drive the step planner (pb_sched_*) over the reference's own
+    ShareGPT-like trace (proj/data/traces/synthetic_sharegpt_200.trace, committed as
+    tests/golden/sharegpt_200_trace.json) with the device tier at ~30% of the working set and
+    a host tier small enough to overflow, so leading chunks get dropped and come back as
+    dropped-prefix recompute spans while other conversations swap in and out.  Returns the
+    window of n_steps consecutive planned steps that carries the most swap-ins, swap-outs and
+    recompute spans (the whole run is planned; the window is the densest stretch of it)."""
     from paper_2312_05516_b200.abi import KvCache
     from paper_2312_05516_b200.planner import Scheduler, default_params
-    from paper_2312_05516_b200.workloads import sharegpt_trace
+    from paper_2312_05516_b200.workloads import reference_trace
 
-    trace = sharegpt_trace(n_conv, seed=5)
+    trace = reference_trace()
     ws = sum((sum(p + o for p, o in turns) + 15) // 16 for _, turns in trace)
-    dev_slots = max(64, int(0.3 * ws))
+    dev_slots = max(64, int(dev_frac * ws))
     host_slots = max(1, int(host_factor * dev_slots))
     cache = KvCache(16, dev_slots, host_slots)
     sched = Scheduler(cache, params=default_params(token_budget=4096))
     pending = [(0.02 * c, c, 0) for c, _ in trace]
     turns = dict(trace)
-    req, req_conv, now, steps, recorded, history = 0, {}, 0.0, 0, [], []
-    while (pending or sched.queue_size or sched.running_size) and steps < 20000 and len(recorded) < n_steps:
+    req, req_conv, now, steps, history = 0, {}, 0.0, 0, []
+    while (pending or sched.queue_size or sched.running_size) and steps < 20000:
         steps += 1
         now += 0.05
         for item in sorted(p for p in pending if p[0] <= now):
@@ -385,36 +504,32 @@ def plan_sharegpt_steps(n_conv: int, n_steps: int, host_factor: float = 0.5, thi
             req_conv[req] = (c, k)
             req += 1
         plans = sched.step(now)
-        for p in plans:
-            history.append(p)
-            if not recorded and p.recompute_tokens > 0:
-                recorded = history[-1:]
-            elif recorded:
-                recorded.append(p)
+        history.extend(plans)
         for i in range(len(plans)):
             for r in sched.complete(i, now + 0.01):
                 c, k = req_conv[r]
                 if k + 1 < len(turns[c]):
                     pending.append((now + think, c, k + 1))  # think time
-    if not recorded:  # no drop happened: first returning turn that swaps in
-        first = next((i for i, p in enumerate(history) if p.in_moves), 0)
-        recorded = history[first:first + n_steps]
-    return recorded, dev_slots, host_slots
+    score = [(len(p.in_moves) > 0) + (len(p.out_moves) > 0) + (p.recompute_tokens > 0) for p in history]
+    n = min(n_steps, len(history))
+    best = max(range(len(history) - n + 1), key=lambda i: sum(score[i:i + n]))
+    return history[best:best + n], dev_slots, host_slots, {"trace_conversations": len(trace),
+                                                           "planned_steps": len(history), "window_start": best}
 
 
-def bench_config5(args):
+def config5_result(args, warmup):
     """Config 5: CPU-tier swap-in/out (pb_swap_step, layer-pipelined) + the ragged attention of
-    the same planned steps, Llama-2-13B shape, one GPU."""
+    the same planned steps, Llama-2-13B shape, one GPU.  Returns the result dict."""
     import torch
 
     from paper_2312_05516_b200 import abi
     from paper_2312_05516_b200.abi import PB_BF16, AttentionPlan, AttnShape, KvTier
 
-    n_layer = args.layers or 40
+    n_layer = 40 if args.config != 5 else (args.layers or 40)
     n_head, n_kv, d, chunk = 40, 10, 128, 16
-    steps, dev_slots, host_slots = plan_sharegpt_steps(args.c5_convs, args.warmup + args.steps)
-    dev = torch.device("cuda", 0)
-    torch.cuda.set_device(dev)
+    c5_steps = max(args.steps, 12)  # at least 12 timed steps (>= 10 of them carry swaps)
+    steps, dev_slots, host_slots, plan_info = plan_sharegpt_steps(warmup + c5_steps)
+    dev = torch.device("cuda", torch.cuda.current_device())
     page_elems = chunk * n_kv * d
     page_bytes = page_elems * 2
     k = torch.empty((n_layer, dev_slots, page_elems), dtype=torch.bfloat16, device=dev)
@@ -447,20 +562,26 @@ def bench_config5(args):
             pl.run(q.data_ptr(), k.data_ptr() + l * layer_stride, v.data_ptr() + l * layer_stride, out.data_ptr(),
                    wsb.data_ptr(), cs.cuda_stream)
 
-    for i in range(args.warmup):
+    for i in range(warmup):
         run(i)
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
-    swap_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
-    clocks = ClockSampler(0)
+    swap_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(c5_steps)]
+    clocks = ClockSampler(dev.index)
     clocks.start()
+    launches0 = abi.launch_count()
     torch.cuda.synchronize()
     t0.record(cs)
-    for s in range(args.steps):
-        run(args.warmup + s, swap_ev[s])
+    for s in range(c5_steps):
+        run(warmup + s, swap_ev[s])
+    # the step's work includes its swap-out D2H (on the tier's own stream)
+    tier.sync()
+    xs.wait_stream(cs)
+    cs.wait_stream(xs)
     t1.record(cs)
     torch.cuda.synchronize()
+    launches = abi.launch_count() - launches0
     clk = clocks.stop()
     total_ms = t0.elapsed_time(t1)
     swap_ms = sum(a.elapsed_time(b) for a, b in swap_ev)
@@ -470,13 +591,14 @@ def bench_config5(args):
         torch.cuda.synchronize()
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(cs)
-        for s in range(args.steps):
-            fn(args.warmup + s)
+        for s in range(c5_steps):
+            fn(warmup + s)
+        tier.sync()
         xs.wait_stream(cs)
         cs.wait_stream(xs)
         b.record(cs)
         torch.cuda.synchronize()
-        return a.elapsed_time(b) / args.steps
+        return a.elapsed_time(b) / c5_steps
 
     def attn_only(i):
         pl = plans[i]
@@ -509,56 +631,70 @@ def bench_config5(args):
                    wsb.data_ptr(), cs.cuda_stream)
         log.mark(abi.PB_EV_STEP_END, -1, -1, cs.cuda_stream)
 
-    for s_ in range(args.steps):
-        audited(args.warmup + s_)
+    for s_ in range(c5_steps):
+        audited(warmup + s_)
+    tier.sync()
     torch.cuda.synchronize()
     events = log.read()
     tier.set_event_log(None)
-    if os.environ.get("PB_CFG5_DUMP"):  # diagnostics: the device-stamped per-layer timeline
-        import numpy as np
-        np.save(os.environ["PB_CFG5_DUMP"], events)
     violations, audited_steps = abi.audit_events(events, per_step=True)
-    timed = steps[args.warmup:args.warmup + args.steps]
-    attn_bytes = sum(pl.stats()["bytes"] for pl in plans[args.warmup:args.warmup + args.steps]) * n_layer
-    attn_flops = sum(pl.stats()["flops"] for pl in plans[args.warmup:args.warmup + args.steps]) * n_layer
+    timed = steps[warmup:warmup + c5_steps]
+    attn_bytes = sum(pl.stats()["bytes"] for pl in plans[warmup:warmup + c5_steps]) * n_layer
+    attn_flops = sum(pl.stats()["flops"] for pl in plans[warmup:warmup + c5_steps]) * n_layer
     n_in = sum(len(p.in_moves) for p in timed)
     n_out = sum(len(p.out_moves) for p in timed)
-    swap_bytes = (n_in + n_out) * tier.chunk_bytes
-    # pinned-copy peaks on this box (1 GiB each way)
-    big = torch.empty(1 << 30, dtype=torch.uint8, device=dev)
-    hbuf = torch.empty(1 << 30, dtype=torch.uint8, pin_memory=True)
-    e = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-    big.copy_(hbuf, non_blocking=True)
-    torch.cuda.synchronize()
-    e[0].record(); big.copy_(hbuf, non_blocking=True); e[1].record()
-    e[2].record(); hbuf.copy_(big, non_blocking=True); e[3].record()
-    torch.cuda.synchronize()
-    h2d_peak = (1 << 30) / (e[0].elapsed_time(e[1]) / 1e3) / 1e9
-    d2h_peak = (1 << 30) / (e[2].elapsed_time(e[3]) / 1e3) / 1e9
+    in_bytes, out_bytes = n_in * tier.chunk_bytes, n_out * tier.chunk_bytes
+    del k, v, q, out, wsb, plans, tier
+    torch.cuda.empty_cache()
+    h2d_peak, d2h_peak = pinned_copy_peaks(torch, dev, 1 << 30)
+    duplex = duplex_microbench(torch, dev)
     peaks, peak_src = load_peaks()
     value = attn_bytes / (total_ms / 1e3) / 1e9
-    line = {
-        "metric": "config 5: ragged paged-attn GB/s with layer-pipelined CPU-tier swap-in/out",
-        "value": value, "unit": "GB/s", "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic ShareGPT-like trace (workloads.sharegpt_trace) planned by pb_sched",
-        "config": {"workload": "cfg5-sharegpt-llama2-13b", "n_layer": n_layer, "conversations": args.c5_convs,
-                   "device_slots": dev_slots, "host_slots": host_slots, "chunk_bytes": tier.chunk_bytes,
-                   "spans_per_step": sum(len(p.spans) for p in timed) / len(timed),
-                   "recompute_tokens": sum(p.recompute_tokens for p in timed)},
+    swap_s = swap_only_ms * c5_steps / 1e3
+    return {
+        "metric": "ragged paged-attn HBM GB/s with layer-pipelined KV swap", "value": value, "unit": "GB/s",
+        "ms_per_step": total_ms / c5_steps, "steps": c5_steps, "warmup": warmup, "n_layer": n_layer,
+        "workload": "cfg5-sharegpt-llama2-13b",
+        "trace": "proj/data/traces/synthetic_sharegpt_200.trace (tests/golden/sharegpt_200_trace.json)",
+        "plan": dict(plan_info, device_slots=dev_slots, host_slots=host_slots, chunk_bytes=page_bytes * 2 * n_layer,
+                     spans_per_step=sum(len(p.spans) for p in timed) / len(timed),
+                     recompute_tokens=sum(p.recompute_tokens for p in timed),
+                     steps_with_swap_in=sum(1 for p in timed if p.in_moves),
+                     steps_with_swap_out=sum(1 for p in timed if p.out_moves),
+                     steps_with_swaps=sum(1 for p in timed if p.in_moves or p.out_moves),
+                     steps_with_recompute=sum(1 for p in timed if p.recompute_tokens)),
         "roofline": {"bound": "hbm", "achieved": value, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": value / peaks["hbm_gbs"], "traffic": None, "peak_source": peak_src,
-                     "tflops": attn_flops / (total_ms / 1e3) / 1e12},
+                     "tflops": attn_flops / (total_ms / 1e3) / 1e12,
+                     "attention_only_gbs": attn_bytes / (attn_only_ms * c5_steps / 1e3) / 1e9,
+                     "attention_only_frac": attn_bytes / (attn_only_ms * c5_steps / 1e3) / 1e9 / peaks["hbm_gbs"]},
         "pipeline_audit": {"violations": violations, "steps": audited_steps,
                            "swap_in_layer_events": int((events["kind"] == abi.PB_EV_SWAP_IN_LAYER).sum()),
                            "attn_start_events": int((events["kind"] == abi.PB_EV_ATTN_START).sum())},
         "parts_ms_per_step": {"attention_only": attn_only_ms, "swap_only": swap_only_ms,
-                              "both": total_ms / args.steps},
-        "swap": {"chunks_in": n_in, "chunks_out": n_out, "bytes": swap_bytes,
-                 "copy_stream_gbs": swap_bytes / (swap_ms / 1e3) / 1e9 if swap_ms > 0 else None,
+                              "both": total_ms / c5_steps},
+        "swap": {"chunks_in": n_in, "chunks_out": n_out, "bytes_in": in_bytes, "bytes_out": out_bytes,
+                 "swap_only_gbs": (in_bytes + out_bytes) / swap_s / 1e9 if swap_s > 0 else None,
+                 "h2d_gbs_swap_only": in_bytes / swap_s / 1e9 if swap_s > 0 else None,
+                 "h2d_frac_of_pinned_peak": in_bytes / swap_s / 1e9 / h2d_peak if swap_s > 0 else None,
+                 "issue_ms": swap_ms,
                  "pinned_h2d_peak_gbs": h2d_peak, "pinned_d2h_peak_gbs": d2h_peak},
-        "clocks": clk,
+        "duplex": duplex,
+        "clocks": clk, "gpu_launches": int(launches),
     }
+
+
+def bench_config5(args):
+    import torch
+    torch.cuda.set_device(0)
+    warmup = max(3, args.warmup)
+    r = config5_result(args, warmup)
+    line = {"metric": r.pop("metric"), "value": r.pop("value"), "unit": r.pop("unit"), "n_gpus": 1,
+            "steps": r.pop("steps"), "warmup": r.pop("warmup"), "ms_per_step": r.pop("ms_per_step"),
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+            "data": "reference ShareGPT trace planned by pb_sched; synthetic KV values",
+            "config": {"workload": r.pop("workload"), "n_layer": r.pop("n_layer")}}
+    line.update(r)
     print(json.dumps(line), flush=True)
     return 0
 
@@ -580,9 +716,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--cpu-budget", type=float, default=12.0, help="seconds of CPU reference work")
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--plan-flags", type=int, default=int(os.environ.get("PB_PLAN_FLAGS", "0")),
-                    help="pb_attn_plan flags (profiling comparisons)")
-    ap.add_argument("--c5-convs", type=int, default=96, help="config 5: conversations in the trace")
+    ap.add_argument("--no-subconfigs", action="store_true", help="headline config only (no cfg2/3/5 sub-results)")
     args = ap.parse_args()
     if args.config == 5:
         if args.impl == "reference":

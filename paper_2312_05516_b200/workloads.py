@@ -24,7 +24,7 @@ from typing import List, Optional, Sequence, Tuple
 
 import numpy as np
 
-from .abi import PB_BF16, PB_F32, AttnShape, Batch
+from .descriptors import PB_BF16, PB_F32, AttnShape, Batch
 
 GOLDEN = 0x9E3779B97F4A7C15
 MASK64 = (1 << 64) - 1
@@ -322,3 +322,17 @@ def sharegpt_trace(n_conv: int, seed: int = 5, mean_turns: float = 5.5, mean_pro
         if turns:
             out.append((c, turns))
     return out
+
+
+def reference_trace(path: Optional[str] = None):
+    """The reference's own ShareGPT-like trace (proj/data/traces/synthetic_sharegpt_200.trace),
+    as committed in tests/golden/sharegpt_200_trace.json by tests/golden/make_trace_fixture.py.
+    Returns [(conv_id, [(prompt, output), ...])] like sharegpt_trace."""
+    import json
+    import os
+    if path is None:
+        path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
+                            "sharegpt_200_trace.json")
+    with open(path) as f:
+        convs = json.load(f)["conversations"]
+    return [(int(c), [(int(p), int(o)) for p, o in turns]) for c, turns in convs]

@@ -248,3 +248,20 @@ def test_page_copy_oracle_roundtrip(oracle):
     oracle.scatter(st, 512, slots, pool2)
     for s in slots:
         assert np.array_equal(pool2[s * 512:(s + 1) * 512], pool[s * 512:(s + 1) * 512])
+
+
+def test_group_oracle_is_the_whole_oracle(oracle):
+    """tests/gpu_helpers.group_oracle (one kv-head group, spans cut into token blocks on
+    host threads) is bit-identical to the whole-batch oracle on those rows: heads are
+    independent (src/attention.cpp:90-92) and a token block is a span of its own."""
+    import gpu_helpers as gh
+    from paper_2312_05516_b200.abi import PB_BF16
+    from paper_2312_05516_b200.workloads import SplitMix64, random_instance
+    rng = SplitMix64(99)
+    w = random_instance(rng, 8, 2, 64, 16, PB_BF16, 4, 300, max_q=150)
+    st, want = oracle.attention(w.shape(), w.batch(), w.host_q(), w.host_pool("k"), w.host_pool("v"))
+    assert st == 0
+    ids = list(range(len(w.spans)))
+    for kvh in range(2):
+        got = gh.group_oracle(oracle, w, ids, kvh, threads=4, block=37)
+        assert np.array_equal(got, gh.group_rows(want, w, ids, kvh))
