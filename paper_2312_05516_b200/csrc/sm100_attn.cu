@@ -89,6 +89,23 @@ constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max gr
 #endif
 
 constexpr int kItemRing = 4; // work items fetched ahead by the TMA warp
+
+// Diagnostics build only (-DPB_TILE_TRACE): per-tile clock64 stamps of the softmax groups and
+// the MMA issuer of the first kTraceCtas CTAs, written after the per-CTA pass records of
+// pb_attn_set_trace (scripts/trace_tiles.py reads them).  Compiles to nothing by default.
+#ifndef PB_TILE_TRACE
+#define PB_TILE_TRACE 0
+#endif
+constexpr int kTraceCtas = 8, kTraceEvents = 1024, kTraceFields = 8;
+__device__ __forceinline__ unsigned long long* tile_trace_slot(unsigned long long* tr, int role, int ev) {
+    if (!PB_TILE_TRACE || !tr || blockIdx.x >= kTraceCtas || ev >= kTraceEvents) return nullptr;
+    return tr + 148 * 2 * 4 + ((static_cast<size_t>(blockIdx.x) * 3 + role) * kTraceEvents + ev) * kTraceFields;
+}
+__device__ __forceinline__ unsigned long long clk64() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    return t;
+}
 constexpr int kMaxPpt = kBN / 8; // pages per kv tile (page_tokens >= 8)
 
 template <int D>
@@ -330,6 +347,7 @@ __global__ void __launch_bounds__(kThreads, 1)
             uint32_t kph = 0, vph = 0;
             uint32_t n_oe[2] = {0, 0};
             uint32_t c_s[2] = {0, 0}, c_p[2] = {0, 0}; // per group: S tiles issued / PV tiles issued
+            int mma_ev = 0;                            // PB_TILE_TRACE event index
             for (;; ++it) {
                 const int slot = it % kItemRing;
                 mbar_wait(&s.item_full[slot], (it / kItemRing) & 1);
@@ -408,8 +426,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                         }
                     }
 #else
+                    unsigned long long* tt = tile_trace_slot(p.trace, 2, mma_ev++);
+                    if (tt) tt[0] = clk64();
                     if (j + 1 < T.n_kv) issue_s(j + 1);
+                    if (tt) tt[1] = clk64();
                     mbar_wait(&s.v_full[vst], vph);
+                    if (tt) tt[2] = clk64();
                     const uint64_t vd = umma_desc_sw128(smem_u32(s.v[vst]), kKvHalf, 1024);
                     for (int t = 0; t < 2; ++t) {
                         if (j >= T.ntiles[t]) continue;
@@ -418,6 +440,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                             ++n_oe[t];
                         }
                         mbar_wait(&s.p_full[t][c_p[t] & 1], (c_p[t] >> 1) & 1);
+                        if (tt) tt[3 + t] = clk64();
                         tc_fence_after();
                         const uint32_t pcol = t * 128 + (c_p[t] & 1) * kBN; // P (bf16) over S
 #pragma unroll
@@ -431,6 +454,13 @@ __global__ void __launch_bounds__(kThreads, 1)
 #endif
                     umma_commit(&s.v_empty[vst]);
                     if (++vst == kKvStages) { vst = 0; vph ^= 1; }
+#if !PB_MMA_POLL
+                    if (tt) {
+                        tt[5] = clk64();
+                        tt[6] = static_cast<unsigned long long>(j);
+                        tt[7] = static_cast<unsigned long long>(item);
+                    }
+#endif
                 }
             }
         }
@@ -498,9 +528,12 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < n_tiles; ++j, ++c_t) {
                 const uint32_t b = c_t & 1;
                 const uint32_t col_s = t * 128 + b * kBN;
+                unsigned long long* tt = (threadIdx.x & 127) == 0 ? tile_trace_slot(p.trace, t, static_cast<int>(c_t)) : nullptr;
+                if (tt) tt[0] = clk64();
                 float x[kCols];
                 {
                     mbar_wait(&s.s_full[t][b], (c_t >> 1) & 1);
+                    if (tt) tt[1] = clk64();
                     tc_fence_after();
                     if (ablate == 1) { // profiling: tensor-core + pipeline bound (P left as S bits)
                         tc_fence_before();
@@ -532,6 +565,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     pair_sync();
                     mt = fmaxf(mt, s.red_m[b][t][hf ^ 1][row]);
                 }
+                if (tt) tt[2] = clk64();
                 const bool grow = mt > m_run + kRescaleThreshold;
                 const float m_new = grow ? mt : m_run;
                 const float corr = grow ? ex2(m_run - m_new) : 1.f;
@@ -569,6 +603,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     ps[(c >> 1) & 3] = add2(ps[(c >> 1) & 3], e);
                     pk[c >> 1] = pack_bf16x2(e.x, e.y);
                 }
+                if (tt) tt[3] = clk64();
                 // P (bf16) over the first kBN/2 columns of this S buffer (this half's share).
                 // Safe against the other half's S columns: both halves loaded their S before
                 // the max exchange above.
@@ -597,6 +632,12 @@ __global__ void __launch_bounds__(kThreads, 1)
                 tmem_st_wait();
                 tc_fence_before();
                 mbar_arrive(&s.p_full[t][b]);
+                if (tt) {
+                    tt[4] = clk64();
+                    tt[5] = rescale ? 1ull : 0ull;
+                    tt[6] = static_cast<unsigned long long>(j);
+                    tt[7] = static_cast<unsigned long long>(item);
+                }
                 const float2 s2 = add2(add2(ps[0], ps[1]), add2(ps[2], ps[3]));
                 const float sum = s2.x + s2.y;
                 l_run = l_run * corr + sum;
