@@ -676,8 +676,13 @@ def config5_result(args, warmup):
         "swap": {"chunks_in": n_in, "chunks_out": n_out, "bytes_in": in_bytes, "bytes_out": out_bytes,
                  "swap_only_gbs": (in_bytes + out_bytes) / swap_s / 1e9 if swap_s > 0 else None,
                  "h2d_gbs_swap_only": in_bytes / swap_s / 1e9 if swap_s > 0 else None,
+                 "d2h_gbs_swap_only": out_bytes / swap_s / 1e9 if swap_s > 0 else None,
                  "h2d_frac_of_pinned_peak": in_bytes / swap_s / 1e9 / h2d_peak if swap_s > 0 else None,
-                 "issue_ms": swap_ms,
+                 "d2h_frac_of_pinned_peak": out_bytes / swap_s / 1e9 / d2h_peak if swap_s > 0 else None,
+                 # the busier direction sets the swap time: its share of the swap-only time
+                 "link_busy_frac": max(in_bytes / h2d_peak, out_bytes / d2h_peak) / 1e9 / swap_s
+                 if swap_s > 0 else None,
+                 "swap_events_ms": swap_ms,
                  "pinned_h2d_peak_gbs": h2d_peak, "pinned_d2h_peak_gbs": d2h_peak},
         "duplex": duplex,
         "clocks": clk, "gpu_launches": int(launches),

@@ -12,13 +12,18 @@
 //     tiles A / B (one TMEM lane = one query row per thread, 208 registers via setmaxnreg),
 //     WG2 = warp 8 TMA producer + warp 9 MMA issuer (one elected thread,
 //     tcgen05.mma.cta_group::1.kind::f16) at 88 registers;
-//   * kv tiles of 64 rows; TMEM: S_A[2] | S_B[2] (64 columns each, double-buffered so S(j+1)
-//     is computed while the softmax turns S(j) into P(j)) | O_A | O_B (128 each).  P (bf16)
-//     is written back over its S buffer with tcgen05.st and fed to the PV MMA from TMEM;
-//   * MMA issue per kv tile j: S_A(j+1), S_B(j+1), then PV_A(j) and PV_B(j) as each group
-//     releases P; one p_full barrier per S buffer lets a group run a tile ahead;
-//   * KV pages are gathered straight from the paged pools by TMA: a 64-row kv tile is
-//     64/page_tokens box loads {64 dims, 1 kv head, page_tokens rows} per 64-dim half at row
+//   * kv tiles of 128 rows, so S = Q K^T runs as M=128 N=128 instructions: at N=64 both
+//     shared-memory operands (6 KB per K=16 step) exceed what the tensor core reads per
+//     clock and the instruction runs at 2/3 rate (scripts/microbench/mma_rate.cu,
+//     profiles/r2_tile_pipeline.md); TMEM: S_A | S_B | O_A | O_B (128 columns each);
+//   * P (bf16) is written back over the first 64 columns of its S buffer with tcgen05.st and
+//     fed to the PV MMA from TMEM; per kv tile j the MMA issuer runs PV_A(j), S_A(j+1),
+//     PV_B(j), S_B(j+1): the tensor pipe executes one thread's MMAs in order, so S_t(j+1)
+//     overwrites P_t(j) only after PV_t(j) has read it, and its completion (s_full) also
+//     proves PV_t(j) done, which is what the lazy O rescale of tile j+1 needs.  Softmax A
+//     overlaps the tensor work of tile B and vice versa (ping-pong);
+//   * KV pages are gathered straight from the paged pools by TMA: a kv tile is
+//     128/page_tokens box loads {64 dims, 1 kv head, page_tokens rows} per 64-dim half at row
 //     block_table[p] * page_tokens (SWIZZLE_128B); pages past the span's table are fetched
 //     out of bounds, which TMA zero-fills;
 //   * O is rescaled lazily (only when a row's running max grows by more than 2^8).
@@ -45,48 +50,52 @@ namespace {
 
 using namespace pb::sm100;
 
-#ifndef PB_SPLIT
-#define PB_SPLIT 0 // 1: two softmax warpgroups per query tile (each takes half of the S columns)
-#endif
-constexpr int kHalves = PB_SPLIT ? 2 : 1;
-constexpr int kSoftWG = 2 * kHalves;          // softmax warpgroups (query tiles A/B x halves)
+constexpr int kSoftWG = 2;                    // softmax warpgroups (query tiles A, B)
 constexpr int kThreads = 128 * (kSoftWG + 1); // + one warpgroup: TMA warp, MMA warp, 2 spare
 constexpr int kProdWarp = 4 * kSoftWG;
 constexpr int kMmaWarp = kProdWarp + 1;
+constexpr int kProdVWarp = kProdWarp + 2; // V tiles have their own producer: K(j+1) is never
+                                          // queued behind a V stage that is still being read
 constexpr int kTileRows = 128;        // M rows per query tile
-constexpr int kBN = 64;               // kv rows per kv tile (N of S = Q K^T, K of O += P V)
-constexpr int kKvStages = 4;          // K ring and V ring depth (kBN-row tiles)
-constexpr uint32_t kTmemCols = 512;   // S_A[2] [0,128) S_B[2] [128,256) O_A [256,384) O_B [384,512)
+constexpr int kBN = 128;              // kv rows per kv tile (N of S = Q K^T, K of O += P V)
+#ifndef PB_K_STAGES
+#define PB_K_STAGES 3
+#endif
+#ifndef PB_V_STAGES
+#define PB_V_STAGES 2
+#endif
+constexpr int kKStages = PB_K_STAGES; // K ring depth (kBN-row tiles): K(j+1) is read first
+constexpr int kVStages = PB_V_STAGES; // V ring depth
+constexpr uint32_t kTmemCols = 512;   // S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512)
 constexpr uint32_t kColO = 256;
 #ifndef PB_SETMAXNREG
 #define PB_SETMAXNREG 1 // 1: rebalance registers, WG2 (TMA + MMA warps) down, softmax groups up
 #endif
 constexpr bool kUseSetMaxNReg = PB_SETMAXNREG != 0;
 #ifndef PB_REG_LO
-#define PB_REG_LO (PB_SPLIT ? 56 : 88) // producer/MMA warpgroup after setmaxnreg.dec
+#define PB_REG_LO 88 // producer/MMA warpgroup after setmaxnreg.dec
 #endif
 #ifndef PB_REG_HI
-#define PB_REG_HI (PB_SPLIT ? 104 : 208) // softmax warpgroups after setmaxnreg.inc
+#define PB_REG_HI 208 // softmax warpgroups after setmaxnreg.inc
 #endif
 // setmaxnreg only moves registers inside the CTA's launch allocation (kThreads x the
 // per-thread count __launch_bounds__ gives, 64K / kThreads rounded down to 8): what the
 // softmax warpgroups gain must be what the producer/MMA warpgroup gives up, or inc blocks
-constexpr int kLaunchRegs = (65536 / (128 * ((PB_SPLIT ? 4 : 2) + 1))) / 8 * 8;
-static_assert((PB_REG_HI - kLaunchRegs) * (PB_SPLIT ? 4 : 2) <= (kLaunchRegs - PB_REG_LO),
+constexpr int kLaunchRegs = (65536 / kThreads) / 8 * 8;
+static_assert((PB_REG_HI - kLaunchRegs) * kSoftWG <= (kLaunchRegs - PB_REG_LO),
               "setmaxnreg budget exceeds the launch register allocation");
 constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max grows by > 2^8
-#ifndef PB_PV_WAIT_EVERY
-#define PB_PV_WAIT_EVERY 0 // 1: the softmax waits for PV(j-1) on every tile, not only to rescale O
-#endif
-#ifndef PB_MMA_POLL
-#define PB_MMA_POLL 0   // 1: MMA warp issues S(j+1) / PV_A(j) / PV_B(j) in readiness order
-#endif
 #ifndef PB_ABLATE_MODE
 #define PB_ABLATE_MODE 0 // roofline ablations, separate builds only: 1 no softmax, 2 no exp2, 5 no P store
 #endif
 #ifndef PB_POLY_EVERY
-#define PB_POLY_EVERY 0 // one exp2 pair in N on the FMA pipe; 0 = all on MUFU (measured fastest, see profiles/)
+#define PB_POLY_EVERY 0 // one exp2 pair in N on the FMA pipe; 0 = all on MUFU
 #endif
+#ifndef PB_P_HALVES
+#define PB_P_HALVES 1 // 1: P released in two 64-column halves, PV of the first half overlaps the
+                      // softmax of the second
+#endif
+constexpr int kPParts = PB_P_HALVES ? 2 : 1;
 
 constexpr int kItemRing = 4; // work items fetched ahead by the TMA warp
 
@@ -111,25 +120,22 @@ constexpr int kMaxPpt = kBN / 8; // pages per kv tile (page_tokens >= 8)
 template <int D>
 struct __align__(1024) Smem {
     uint8_t q[2][kTileRows * D * 2];      // tiles A, B: [D/64][128 rows][128 B] K-major SW128
-    uint8_t k[kKvStages][kBN * D * 2];    // ring of kv tiles: [D/64][64 rows][128 B] K-major SW128
-    uint8_t v[kKvStages][kBN * D * 2];    // same layout, read as the MN-major SW128 B operand
+    uint8_t k[kKStages][kBN * D * 2];     // ring of kv tiles: [D/64][128 rows][128 B] K-major SW128
+    uint8_t v[kVStages][kBN * D * 2];     // same layout, read as the MN-major SW128 B operand
     uint64_t q_full, q_empty;             // Q is released after the item's last S MMA
-    uint64_t k_full[kKvStages], k_empty[kKvStages], v_full[kKvStages], v_empty[kKvStages];
-    uint64_t s_full[2][2];                // [query tile][S buffer]
-    uint64_t p_full[2][2];                // [query tile][S buffer]: P released (one barrier per
-                                          // buffer, so the softmax can run a tile ahead of the
-                                          // MMA warp without lapping a barrier phase)
-    uint64_t pv_done[2], o_ready[2], o_empty[2]; // per query tile
+    uint64_t k_full[kKStages], k_empty[kKStages], v_full[kVStages], v_empty[kVStages];
+    uint64_t s_full[2];                   // [query tile] S landed
+    uint64_t p_full[2][kPParts];          // [query tile][column part] P stored (O rescaled
+                                          // before the first part)
+    uint64_t o_ready[2], o_empty[2];      // per query tile
     uint64_t item_full[kItemRing], item_empty[kItemRing];   // dynamic tile scheduler ring
     uint64_t drain;                       // MMA issuer: every commit of the pass has landed
     int32_t item_ring[kItemRing];
-    float red_m[2][2][kHalves][128];      // [S buffer][query tile][half][row] partial row max
-    float red_l[2][kHalves][128];         // [query tile][half][row] partial row sum
 };
 
 // one CTA per SM: the larger of the two layouts plus 1 KiB of alignment slack must fit the
 // 227 KiB opt-in shared memory of an sm_100 CTA
-static_assert(sizeof(Smem<128>) + 1024 <= 232448, "tile layout exceeds shared memory");
+static_assert(sizeof(Smem<128>) + 1024 + 64 <= 232448, "tile layout exceeds shared memory");
 static_assert(sizeof(dtc::DtSmem) + 1024 <= 232448, "decode layout exceeds shared memory");
 
 __device__ __forceinline__ int ceil_div(int a, int b) { return (a + b - 1) / b; }
@@ -166,24 +172,23 @@ template <int D>
 __device__ __forceinline__ void tile_init(Smem<D>& s) { // thread 0
     mbar_init(&s.q_full, 1);
     mbar_init(&s.q_empty, 1);
-    for (int i = 0; i < kKvStages; ++i) {
+    for (int i = 0; i < kKStages; ++i) {
         mbar_init(&s.k_full[i], 1);
         mbar_init(&s.k_empty[i], 1);
+    }
+    for (int i = 0; i < kVStages; ++i) {
         mbar_init(&s.v_full[i], 1);
         mbar_init(&s.v_empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
-        mbar_init(&s.s_full[i][0], 1);
-        mbar_init(&s.s_full[i][1], 1);
-        mbar_init(&s.p_full[i][0], 128 * kHalves);
-        mbar_init(&s.p_full[i][1], 128 * kHalves);
-        mbar_init(&s.pv_done[i], 1);
+        mbar_init(&s.s_full[i], 1);
+        for (int h = 0; h < kPParts; ++h) mbar_init(&s.p_full[i][h], 128);
         mbar_init(&s.o_ready[i], 1);
-        mbar_init(&s.o_empty[i], 128 * kHalves);
+        mbar_init(&s.o_empty[i], 128);
     }
     for (int i = 0; i < kItemRing; ++i) {
         mbar_init(&s.item_full[i], 1);
-        mbar_init(&s.item_empty[i], 1 + 4 * kSoftWG); // MMA thread + the softmax warps
+        mbar_init(&s.item_empty[i], 2 + 4 * kSoftWG); // MMA thread, V producer + the softmax warps
     }
     mbar_init(&s.drain, 1);
 }
@@ -276,39 +281,50 @@ __global__ void __launch_bounds__(kThreads, 1)
         if constexpr (D == 128)
             dtc::decode_cta_run<GD>(ds, tmem, &tm_qd, &tm_k, &tm_v, p, p.dec_items, p.n_dec_items, ctr + 4, kProdWarp,
                                     kMmaWarp, 0, kProdWarp + 2);
-    } else if (warp == kProdWarp) {
-        // ============================ TMA producer ============================
+    } else if (warp == kProdWarp || warp == kProdVWarp) {
+        // ===================== TMA producers (K warp: Q + K, V warp: V) =====================
         if (elect_one()) {
-            int it = 0, kst = 0, vst = 0;
-            uint32_t kph = 0, vph = 0;
+            const bool kw = warp == kProdWarp;
+            int it = 0, st = 0;
+            uint32_t ph = 0;
+            const int n_st = kw ? kKStages : kVStages;
             const uint32_t q_bytes = KH * 128u * static_cast<uint32_t>(g * tpt);
             const int oob_row = p.n_slots * chunk;
-            // Dynamic tile scheduler: the TMA warp takes the next item (items are in LPT order)
-            // from a global ticket when it is ready to load it, and hands the index to the MMA
-            // and softmax roles through a small shared ring.
+            // Dynamic tile scheduler: the K warp takes the next item (items are in LPT order)
+            // from a global ticket when it is ready to load it, and hands the index to the MMA,
+            // V and softmax roles through a small shared ring.
             int* ticket = p.work_counter + 2; // [2] next tile item (reset by the last CTA to retire)
             for (;; ++it) {
                 const int slot = it % kItemRing;
-                if (it >= kItemRing) mbar_wait(&s.item_empty[slot], ((it / kItemRing) - 1) & 1);
-                int item = atomicAdd(ticket, 1);
-                if (item >= p.n_items) item = -1;
-                s.item_ring[slot] = item;
-                mbar_arrive(&s.item_full[slot]);
+                int item;
+                if (kw) {
+                    if (it >= kItemRing) mbar_wait(&s.item_empty[slot], ((it / kItemRing) - 1) & 1);
+                    item = atomicAdd(ticket, 1);
+                    if (item >= p.n_items) item = -1;
+                    s.item_ring[slot] = item;
+                    mbar_arrive(&s.item_full[slot]);
+                } else {
+                    mbar_wait(&s.item_full[slot], (it / kItemRing) & 1);
+                    item = *reinterpret_cast<volatile int32_t*>(&s.item_ring[slot]);
+                    mbar_arrive(&s.item_empty[slot]);
+                }
                 if (item < 0) break;
                 const WorkItem w = p.items[item];
                 const SpanDev sp = p.spans[w.span];
-                if (it > 0) mbar_wait(&s.q_empty, (it - 1) & 1);
                 const ItemTiles T = item_tiles(w, sp, tpt);
-                mbar_arrive_expect_tx(&s.q_full, q_bytes * (T.nt[1] > 0 ? 2u : 1u));
-                for (int t = 0; t < 2; ++t)
-                    if (T.nt[t] > 0)
-                        for (int h = 0; h < KH; ++h)
-                            tma_load_3d(s.q[t] + h * kHalfBytes, &tm_q, &s.q_full, h * 64, w.kvh * g,
-                                        sp.query_start + w.t0 + t * tpt);
+                if (kw) {
+                    if (it > 0) mbar_wait(&s.q_empty, (it - 1) & 1);
+                    mbar_arrive_expect_tx(&s.q_full, q_bytes * (T.nt[1] > 0 ? 2u : 1u));
+                    for (int t = 0; t < 2; ++t)
+                        if (T.nt[t] > 0)
+                            for (int h = 0; h < KH; ++h)
+                                tma_load_3d(s.q[t] + h * kHalfBytes, &tm_q, &s.q_full, h * 64, w.kvh * g,
+                                            sp.query_start + w.t0 + t * tpt);
+                }
                 const int32_t* table = p.block_tables + sp.bt_off;
                 const int n_pages = sp.n_pages;
-                const int n_kv = T.n_kv;
-                for (int j = 0; j < n_kv; ++j) {
+                const CUtensorMap* tm = kw ? &tm_k : &tm_v;
+                for (int j = 0; j < T.n_kv; ++j) {
                     // the tile's block-table entries: independent loads issued together, before
                     // any barrier wait or TMA (one L2 round trip per tile, not one per page)
                     int rows[kMaxPpt];
@@ -317,24 +333,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                         const int page = j * ppt + pg;
                         rows[pg] = (pg < ppt && page < n_pages) ? __ldg(table + page) * chunk : oob_row;
                     }
-                    for (int which = 0; which < 2; ++which) {
-                        uint64_t* full = which ? &s.v_full[vst] : &s.k_full[kst];
-                        uint64_t* empty = which ? &s.v_empty[vst] : &s.k_empty[kst];
-                        uint8_t* dst = which ? s.v[vst] : s.k[kst];
-                        const CUtensorMap* tm = which ? &tm_v : &tm_k;
-                        mbar_wait(empty, (which ? vph : kph) ^ 1);
-                        mbar_arrive_expect_tx(full, kKvTileBytes);
+                    uint64_t* full = kw ? &s.k_full[st] : &s.v_full[st];
+                    uint8_t* dst = kw ? s.k[st] : s.v[st];
+                    mbar_wait(kw ? &s.k_empty[st] : &s.v_empty[st], ph ^ 1);
+                    mbar_arrive_expect_tx(full, kKvTileBytes);
 #pragma unroll
-                        for (int pg = 0; pg < kMaxPpt; ++pg)
-                            if (pg < ppt)
-                                for (int h = 0; h < KH; ++h)
-                                    tma_load_3d(dst + h * kKvHalf + pg * chunk * 128, tm, full, h * 64, w.kvh, rows[pg]);
-                        if (which) {
-                            if (++vst == kKvStages) { vst = 0; vph ^= 1; }
-                        } else {
-                            if (++kst == kKvStages) { kst = 0; kph ^= 1; }
-                        }
-                    }
+                    for (int pg = 0; pg < kMaxPpt; ++pg)
+                        if (pg < ppt)
+                            for (int h = 0; h < KH; ++h)
+                                tma_load_3d(dst + h * kKvHalf + pg * chunk * 128, tm, full, h * 64, w.kvh, rows[pg]);
+                    if (++st == n_st) { st = 0; ph ^= 1; }
                 }
             }
         }
@@ -346,8 +354,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             int it = 0, kst = 0, vst = 0;
             uint32_t kph = 0, vph = 0;
             uint32_t n_oe[2] = {0, 0};
-            uint32_t c_s[2] = {0, 0}, c_p[2] = {0, 0}; // per group: S tiles issued / PV tiles issued
-            int mma_ev = 0;                            // PB_TILE_TRACE event index
+            uint32_t c_p[2] = {0, 0}; // per group: PV tiles issued (p_full phase)
+            int mma_ev = 0;           // PB_TILE_TRACE event index
             for (;; ++it) {
                 const int slot = it % kItemRing;
                 mbar_wait(&s.item_full[slot], (it / kItemRing) & 1);
@@ -364,103 +372,74 @@ __global__ void __launch_bounds__(kThreads, 1)
                 const ItemTiles T = item_tiles(w, sp, tpt);
                 mbar_wait(&s.q_full, it & 1);
                 tc_fence_after();
-                // S_t(jj) = Q_t K(jj)^T into group t's S buffer (c_s[t] & 1), for every group that
-                // needs kv tile jj.  Descriptors are advanced by adding (byte offset >> 4) to the
-                // start-address field (no carry: shared addresses < 256 KB).
-                auto issue_s = [&](int jj) {
-                    mbar_wait(&s.k_full[kst], kph);
-                    tc_fence_after();
-                    const uint64_t kd = umma_desc_sw128(smem_u32(s.k[kst]), 16, 1024);
-                    for (int t = 0; t < 2; ++t) {
-                        if (jj >= T.ntiles[t]) continue;
-                        const uint64_t qd = umma_desc_sw128(smem_u32(s.q[t]), 16, 1024);
-                        const uint32_t b = c_s[t] & 1;
+                // S_t = Q_t K^T (K stage ks) into group t's S buffer.  Descriptors are advanced
+                // by adding (byte offset >> 4) to the start-address field (no carry: shared
+                // addresses < 256 KB).
+                auto issue_s = [&](int t, int ks) {
+                    const uint64_t kd = umma_desc_sw128(smem_u32(s.k[ks]), 16, 1024);
+                    const uint64_t qd = umma_desc_sw128(smem_u32(s.q[t]), 16, 1024);
 #pragma unroll
-                        for (int kk = 0; kk < D / 16; ++kk) {
-                            const uint32_t oq = ((kk >> 2) * kHalfBytes + (kk & 3) * 32) >> 4;
-                            const uint32_t ok = ((kk >> 2) * kKvHalf + (kk & 3) * 32) >> 4;
-                            umma_bf16_ss(tmem + t * 128 + b * kBN, qd + oq, kd + ok, idesc_s, kk > 0);
-                        }
-                        umma_commit(&s.s_full[t][b]);
-                        ++c_s[t];
+                    for (int kk = 0; kk < D / 16; ++kk) {
+                        const uint32_t oq = ((kk >> 2) * kHalfBytes + (kk & 3) * 32) >> 4;
+                        const uint32_t ok = ((kk >> 2) * kKvHalf + (kk & 3) * 32) >> 4;
+                        umma_bf16_ss(tmem + t * 128, qd + oq, kd + ok, idesc_s, kk > 0);
                     }
-                    umma_commit(&s.k_empty[kst]);
-                    if (++kst == kKvStages) { kst = 0; kph ^= 1; }
-                    if (jj + 1 == T.n_kv) umma_commit(&s.q_empty); // Q is read by S MMAs only
+                    umma_commit(&s.s_full[t]);
                 };
-                // S runs one kv tile ahead of PV: S(j+1) is computed while the softmax groups
-                // turn S(j) into P(j) (two S buffers per group)
-                // S(j) for both groups of the first kv tile needs K(0) before anything else
-                issue_s(0);
+                // prologue: S_A(0), S_B(0) from K(0)
+                mbar_wait(&s.k_full[kst], kph);
+                tc_fence_after();
+                for (int t = 0; t < 2; ++t)
+                    if (T.ntiles[t] > 0) issue_s(t, kst);
+                umma_commit(&s.k_empty[kst]);
+                if (++kst == kKStages) { kst = 0; kph ^= 1; }
+                if (T.n_kv == 1) umma_commit(&s.q_empty); // Q is read by S MMAs only
                 for (int j = 0; j < T.n_kv; ++j) {
-#if PB_MMA_POLL
-                    // issue S(j+1), PV_A(j), PV_B(j) in whatever order their inputs become ready
-                    bool s_next = j + 1 >= T.n_kv;
-                    bool pv[2] = {j >= T.ntiles[0], j >= T.ntiles[1]};
-                    bool v_in = false;
+                    unsigned long long* tt = tile_trace_slot(p.trace, 2, mma_ev++);
+                    if (tt) tt[0] = clk64();
+                    const bool nxt = j + 1 < T.n_kv;
+                    if (nxt) mbar_wait(&s.k_full[kst], kph);
+                    if (tt) tt[1] = clk64();
+                    mbar_wait(&s.v_full[vst], vph);
+                    if (tt) tt[2] = clk64();
+                    tc_fence_after();
                     const uint64_t vd = umma_desc_sw128(smem_u32(s.v[vst]), kKvHalf, 1024);
-                    while (!(s_next && pv[0] && pv[1])) {
-                        if (!s_next && mbar_try_wait(smem_u32(&s.k_full[kst]), kph)) {
-                            issue_s(j + 1);
-                            s_next = true;
-                        }
-                        if (!v_in) v_in = mbar_try_wait(smem_u32(&s.v_full[vst]), vph);
-                        if (!v_in) continue;
-                        for (int t = 0; t < 2; ++t) {
-                            if (pv[t] || !mbar_try_wait(smem_u32(&s.p_full[t][c_p[t] & 1]), (c_p[t] >> 1) & 1))
-                                continue;
+                    for (int t = 0; t < 2; ++t) {
+                        if (j < T.ntiles[t]) {
                             if (j == 0) {
                                 mbar_wait(&s.o_empty[t], (n_oe[t] & 1) ^ 1);
                                 ++n_oe[t];
                             }
-                            tc_fence_after();
-                            const uint32_t pcol = t * 128 + (c_p[t] & 1) * kBN;
+                            const uint32_t pcol = t * 128; // P (bf16) over the first 64 S columns
 #pragma unroll
-                            for (int kk = 0; kk < kBN / 16; ++kk)
-                                umma_bf16_ts(tmem + kColO + t * 128, tmem + pcol + kk * 8, vd + kk * (2048 >> 4),
-                                             idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+                            for (int h = 0; h < kPParts; ++h) {
+                                mbar_wait(&s.p_full[t][h], c_p[t] & 1);
+                                if (tt && h == kPParts - 1) tt[3 + t] = clk64();
+                                tc_fence_after();
+#pragma unroll
+                                for (int kk = h * (kBN / 16 / kPParts); kk < (h + 1) * (kBN / 16 / kPParts); ++kk)
+                                    umma_bf16_ts(tmem + kColO + t * 128, tmem + pcol + kk * 8,
+                                                 vd + kk * (2048 >> 4), idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
+                            }
                             ++c_p[t];
-                            umma_commit(&s.pv_done[t]);
                             if (j + 1 == T.ntiles[t]) umma_commit(&s.o_ready[t]);
-                            pv[t] = true;
                         }
+                        // S_t(j+1) behind PV_t(j) on the in-order tensor pipe (P_t(j) lives in
+                        // the S_t columns)
+                        if (nxt && j + 1 < T.ntiles[t]) issue_s(t, kst);
                     }
-#else
-                    unsigned long long* tt = tile_trace_slot(p.trace, 2, mma_ev++);
-                    if (tt) tt[0] = clk64();
-                    if (j + 1 < T.n_kv) issue_s(j + 1);
-                    if (tt) tt[1] = clk64();
-                    mbar_wait(&s.v_full[vst], vph);
-                    if (tt) tt[2] = clk64();
-                    const uint64_t vd = umma_desc_sw128(smem_u32(s.v[vst]), kKvHalf, 1024);
-                    for (int t = 0; t < 2; ++t) {
-                        if (j >= T.ntiles[t]) continue;
-                        if (j == 0) {
-                            mbar_wait(&s.o_empty[t], (n_oe[t] & 1) ^ 1);
-                            ++n_oe[t];
-                        }
-                        mbar_wait(&s.p_full[t][c_p[t] & 1], (c_p[t] >> 1) & 1);
-                        if (tt) tt[3 + t] = clk64();
-                        tc_fence_after();
-                        const uint32_t pcol = t * 128 + (c_p[t] & 1) * kBN; // P (bf16) over S
-#pragma unroll
-                        for (int kk = 0; kk < kBN / 16; ++kk)
-                            umma_bf16_ts(tmem + kColO + t * 128, tmem + pcol + kk * 8, vd + kk * (2048 >> 4),
-                                         idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
-                        ++c_p[t];
-                        umma_commit(&s.pv_done[t]);
-                        if (j + 1 == T.ntiles[t]) umma_commit(&s.o_ready[t]);
-                    }
-#endif
                     umma_commit(&s.v_empty[vst]);
-                    if (++vst == kKvStages) { vst = 0; vph ^= 1; }
-#if !PB_MMA_POLL
+                    if (++vst == kVStages) { vst = 0; vph ^= 1; }
+                    if (nxt) {
+                        umma_commit(&s.k_empty[kst]);
+                        if (++kst == kKStages) { kst = 0; kph ^= 1; }
+                        if (j + 2 == T.n_kv) umma_commit(&s.q_empty);
+                    }
                     if (tt) {
                         tt[5] = clk64();
                         tt[6] = static_cast<unsigned long long>(j);
                         tt[7] = static_cast<unsigned long long>(item);
                     }
-#endif
                 }
             }
         }
@@ -479,28 +458,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                                     kMmaWarp, 0, kProdWarp + 2);
     } else {
         // ============ softmax / correction / epilogue (one group per query tile) ============
-        // kHalves softmax warpgroups per query tile: warpgroup wg serves tile wg & 1 and the
-        // column half wg >> 1 of every S tile (same TMEM lanes, different columns); the two
-        // halves of a row agree on the running max through shared memory once per tile.
-        const int t = wg & 1;                       // query tile of this warpgroup
-        const int hf = wg >> 1;                     // column half (0 when kHalves == 1)
+        const int t = wg;                           // query tile of this warpgroup
         const int quad = warp & 3;                  // TMEM lane quadrant of this warp
         const int row = quad * 32 + (threadIdx.x & 31);
         const uint32_t t_lane = tmem + (static_cast<uint32_t>(quad * 32) << 16);
+        const uint32_t col_s = t * 128;
         const uint32_t col_o = kColO + t * 128;
-        constexpr int kCols = kBN / kHalves;        // S columns per thread per kv tile
-        constexpr int kOCols = D / kHalves;         // O columns per thread (rescale, epilogue)
         const float sl2 = p.scale_log2;
         // roofline ablations exist only in builds with -DPB_ABLATE_MODE=n
         // (scripts/build_variants.sh); the production kernel carries no checks for them
         constexpr int ablate = PB_ABLATE_MODE;
         uint32_t n_o = 0;
-        uint32_t c_t = 0;     // kv tiles processed by this group (S buffer / barrier phase)
+        uint32_t c_t = 0;     // kv tiles processed by this group (s_full / p_full phase)
         uint32_t kv_seen = 0; // kv tiles loaded for earlier items (V ring position)
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
-        auto pair_sync = [&]() { // the two warps (one per half) that own these 32 rows
-            if constexpr (kHalves > 1) asm volatile("bar.sync %0, 64;" ::"r"(1 + t * 4 + quad) : "memory");
-        };
         for (int it = 0;; ++it) {
             const int slot = it % kItemRing;
             mbar_wait(&s.item_full[slot], (it / kItemRing) & 1);
@@ -519,60 +490,54 @@ __global__ void __launch_bounds__(kThreads, 1)
             // never-written pool memory): this group zeroes them in the V stage of the item's
             // last kv tile before its PV reads it (tile A when it reaches that tile, else B),
             // so 0 * NaN cannot reach O
-            const bool zero_owner = hf == 0 && ((t == 0) ? (T.ntiles[0] == T.n_kv) : (T.ntiles[0] < T.n_kv));
+            const bool zero_owner = (t == 0) ? (T.ntiles[0] == T.n_kv) : (T.ntiles[0] < T.n_kv);
             const int t_local = row / g;
             const bool valid = t_local < T.nt[t] && row < g * tpt;
             const int tok0 = w.t0 + t * tpt;           // first span-relative token of this tile
             const int allowed = sp.causal_offset + tok0 + (valid ? t_local : 0) + 1;
             float m_run = -CUDART_INF_F, l_run = 0.f;
             for (int j = 0; j < n_tiles; ++j, ++c_t) {
-                const uint32_t b = c_t & 1;
-                const uint32_t col_s = t * 128 + b * kBN;
                 unsigned long long* tt = (threadIdx.x & 127) == 0 ? tile_trace_slot(p.trace, t, static_cast<int>(c_t)) : nullptr;
                 if (tt) tt[0] = clk64();
-                float x[kCols];
-                {
-                    mbar_wait(&s.s_full[t][b], (c_t >> 1) & 1);
-                    if (tt) tt[1] = clk64();
-                    tc_fence_after();
-                    if (ablate == 1) { // profiling: tensor-core + pipeline bound (P left as S bits)
-                        tc_fence_before();
-                        mbar_arrive(&s.p_full[t][b]);
-                        l_run = 1.f;
-                        continue;
-                    }
-#pragma unroll
-                    for (int c = 0; c < kCols / 32; ++c)
-                        tmem_ld32(t_lane + col_s + hf * kCols + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
-                    tmem_ld_wait();
+                float x[kBN];
+                mbar_wait(&s.s_full[t], c_t & 1);
+                if (tt) tt[1] = clk64();
+                tc_fence_after();
+                if (ablate == 1) { // profiling: tensor-core + pipeline bound (P left as S bits)
+                    tc_fence_before();
+                    for (int h = 0; h < kPParts; ++h) mbar_arrive(&s.p_full[t][h]);
+                    l_run = 1.f;
+                    continue;
                 }
-                const int kv0 = j * kBN + hf * kCols;
-                const bool diag = kv0 + kCols > allowed;
-                float pm[8];
+#pragma unroll
+                for (int c = 0; c < kBN / 32; ++c)
+                    tmem_ld32(t_lane + col_s + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&x[c * 32]));
+                tmem_ld_wait();
+                const int kv0 = j * kBN;
                 // causal mask (only tiles that cross this row's boundary) + running max
-                if (diag) {
+                if (kv0 + kBN > allowed) {
 #pragma unroll
-                    for (int c = 0; c < kCols; ++c) x[c] = (kv0 + c < allowed) ? x[c] : -CUDART_INF_F;
+                    for (int c = 0; c < kBN; ++c) x[c] = (kv0 + c < allowed) ? x[c] : -CUDART_INF_F;
                 }
+                float pm[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u) pm[u] = x[u];
 #pragma unroll
-                for (int c = 8; c < kCols; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
-                float mt = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
-                                 fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * sl2;
-                if constexpr (kHalves > 1) {
-                    s.red_m[b][t][hf][row] = mt;
-                    pair_sync();
-                    mt = fmaxf(mt, s.red_m[b][t][hf ^ 1][row]);
-                }
+                for (int c = 8; c < kBN; ++c) pm[c & 7] = fmaxf(pm[c & 7], x[c]);
+                const float mt = fmaxf(fmaxf(fmaxf(pm[0], pm[1]), fmaxf(pm[2], pm[3])),
+                                       fmaxf(fmaxf(pm[4], pm[5]), fmaxf(pm[6], pm[7]))) * sl2;
                 if (tt) tt[2] = clk64();
                 const bool grow = mt > m_run + kRescaleThreshold;
                 const float m_new = grow ? mt : m_run;
                 const float corr = grow ? ex2(m_run - m_new) : 1.f;
-                if (zero_owner && j + 1 == T.n_kv && row < kBN) {
+                if (zero_owner && j + 1 == T.n_kv) {
                     const int kv = j * kBN + row;
                     if (kv >= sp.context_len && kv < sp.n_pages * chunk) {
-                        uint8_t* vrow = s.v[(kv_base + j) % kKvStages] + row * 128;
+                        // the V tile must have landed first (S_t(j) landing does not imply it);
+                        // its stage cannot be refilled before this group releases P_t(j)
+                        const uint32_t vt = kv_base + j;
+                        mbar_wait(&s.v_full[vt % kVStages], (vt / kVStages) & 1);
+                        uint8_t* vrow = s.v[vt % kVStages] + row * 128;
 #pragma unroll
                         for (int h = 0; h < KH; ++h)
 #pragma unroll
@@ -581,58 +546,56 @@ __global__ void __launch_bounds__(kThreads, 1)
                         fence_proxy_async_smem();
                     }
                 }
-                float2 ps[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) ps[u] = make_float2(0.f, 0.f);
-                uint32_t pk[kCols / 2];
-                const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_new, -m_new);
-#pragma unroll
-                for (int c = 0; c < kCols; c += 2) {
-                    // exp2((s - max) * log2e / scale) on packed pairs (FFMA2 / FADD2) and MUFU
-                    const float2 a = fma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
-                    float2 e;
-                    if (ablate == 2) { // profiling: no exponentials
-                        e = a;
-                    } else if (PB_POLY_EVERY > 0 && ((c >> 1) % (PB_POLY_EVERY > 0 ? PB_POLY_EVERY : 1)) ==
-                                                        PB_POLY_EVERY - 1) {
-                        e = exp2_neg_poly_x2(a);
-                    } else {
-                        e.x = ex2(a.x);
-                        e.y = ex2(a.y);
-                    }
-                    ps[(c >> 1) & 3] = add2(ps[(c >> 1) & 3], e);
-                    pk[c >> 1] = pack_bf16x2(e.x, e.y);
-                }
-                if (tt) tt[3] = clk64();
-                // P (bf16) over the first kBN/2 columns of this S buffer (this half's share).
-                // Safe against the other half's S columns: both halves loaded their S before
-                // the max exchange above.
-                if (ablate != 5) {
-                    if constexpr (kCols == 64) tmem_st32(t_lane + col_s, *reinterpret_cast<uint32_t(*)[32]>(pk));
-                    else dtc::tmem_st16(t_lane + col_s + hf * (kCols / 2), *reinterpret_cast<uint32_t(*)[16]>(pk));
-                }
-                // O_t may only be rescaled once PV_t of the previous tile is complete.  The
-                // parity wait is exact without waiting every tile: S_t(j) landed, and it was
-                // issued after PV_t(j-2) on the in-order tensor pipe, so pv_done is at most
-                // one phase behind (PV_t(j) cannot start before this thread releases P_t(j)).
+                // lazy O rescale, before any part of P(j) is released to PV_t(j): S_t(j)
+                // completing proves PV_t(j-1) done (in-order pipe)
                 const bool rescale = j > 0 && __any_sync(0xffffffffu, grow);
-                if (PB_PV_WAIT_EVERY ? c_t > 0 : rescale) mbar_wait(&s.pv_done[t], (c_t - 1) & 1);
                 if (rescale) {
-                    tc_fence_after();
 #pragma unroll
-                    for (int c = 0; c < kOCols / 32; ++c) {
+                    for (int c = 0; c < D / 32; ++c) {
                         uint32_t o[32];
-                        tmem_ld32(t_lane + col_o + hf * kOCols + c * 32, o);
+                        tmem_ld32(t_lane + col_o + c * 32, o);
                         tmem_ld_wait();
 #pragma unroll
                         for (int e = 0; e < 32; ++e) o[e] = __float_as_uint(__uint_as_float(o[e]) * corr);
-                        tmem_st32(t_lane + col_o + hf * kOCols + c * 32, o);
+                        tmem_st32(t_lane + col_o + c * 32, o);
                     }
                 }
-                tmem_st_wait();
-                tc_fence_before();
-                mbar_arrive(&s.p_full[t][b]);
+                float2 ps[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) ps[u] = make_float2(0.f, 0.f);
+                const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_new, -m_new);
+#pragma unroll
+                for (int h = 0; h < kPParts; ++h) {
+#pragma unroll
+                    for (int c0 = h * (kBN / kPParts); c0 < (h + 1) * (kBN / kPParts); c0 += 32) {
+                        uint32_t pk[16];
+#pragma unroll
+                        for (int c = c0; c < c0 + 32; c += 2) {
+                            // exp2((s - max) * log2e / scale) on packed pairs (FFMA2 / FADD2) and MUFU
+                            const float2 a = fma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
+                            float2 e;
+                            if (ablate == 2) { // profiling: no exponentials
+                                e = a;
+                            } else if (PB_POLY_EVERY > 0 &&
+                                       ((c >> 1) % (PB_POLY_EVERY > 0 ? PB_POLY_EVERY : 1)) == PB_POLY_EVERY - 1) {
+                                e = exp2_neg_poly_x2(a);
+                            } else {
+                                e.x = ex2(a.x);
+                                e.y = ex2(a.y);
+                            }
+                            ps[(c >> 1) & 3] = add2(ps[(c >> 1) & 3], e);
+                            pk[(c - c0) >> 1] = pack_bf16x2(e.x, e.y);
+                        }
+                        // P (bf16) over the first 64 columns of this S buffer (all of S is in
+                        // registers already)
+                        if (ablate != 5) dtc::tmem_st16(t_lane + col_s + (c0 >> 1), pk);
+                    }
+                    tmem_st_wait();
+                    tc_fence_before();
+                    mbar_arrive(&s.p_full[t][h]);
+                }
                 if (tt) {
+                    tt[3] = clk64();
                     tt[4] = clk64();
                     tt[5] = rescale ? 1ull : 0ull;
                     tt[6] = static_cast<unsigned long long>(j);
@@ -643,23 +606,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 l_run = l_run * corr + sum;
                 m_run = m_new;
             }
-            // epilogue: O / l -> bf16 -> global (this half's O columns)
+            // epilogue: O / l -> bf16 -> global
             mbar_wait(&s.o_ready[t], n_o & 1);
             ++n_o;
             tc_fence_after();
-            if constexpr (kHalves > 1) {
-                s.red_l[t][hf][row] = l_run;
-                pair_sync();
-                l_run += s.red_l[t][hf ^ 1][row];
-            }
             const float inv_l = 1.f / l_run;
             const int h = w.kvh * g + (row % g);
-            __nv_bfloat16* orow =
-                out + (static_cast<size_t>(sp.query_start + tok0 + t_local) * p.n_head + h) * D + hf * kOCols;
+            __nv_bfloat16* orow = out + (static_cast<size_t>(sp.query_start + tok0 + t_local) * p.n_head + h) * D;
 #pragma unroll
-            for (int c = 0; c < kOCols / 32; ++c) {
+            for (int c = 0; c < D / 32; ++c) {
                 uint32_t o[32];
-                tmem_ld32(t_lane + col_o + hf * kOCols + c * 32, o);
+                tmem_ld32(t_lane + col_o + c * 32, o);
                 tmem_ld_wait();
                 if (valid) {
 #pragma unroll
@@ -694,6 +651,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_dealloc<kTmemCols>(tmem);
     }
 }
+
 
 // ------------------------------------------------------------------ host side
 
