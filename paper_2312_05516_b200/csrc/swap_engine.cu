@@ -122,17 +122,9 @@ __global__ void __launch_bounds__(256) swap_scatter_block_kernel(const uint8_t* 
 
 int n_sms() { return device_sms(); }
 
-// Batched copies (one driver call per batch, cudaMemcpyBatchAsync); per-copy fallback if the
-// runtime refuses the batch.
+// One cudaMemcpyAsync per copy, in list order on one stream.  (The driver's batched-copy
+// entry point faulted the GPU on this driver/part, so it is not used.)
 void copy_batch(std::vector<void*>& dst, std::vector<void*>& src, std::vector<size_t>& sizes, cudaStream_t st) {
-    if (dst.empty()) return;
-    cudaMemcpyAttributes attr{};
-    attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-    size_t attr_idx = 0, fail_idx = 0;
-    cudaError_t e = cudaMemcpyBatchAsync(dst.data(), src.data(), sizes.data(), dst.size(), &attr, &attr_idx, 1,
-                                         &fail_idx, st);
-    if (e == cudaSuccess) return;
-    cudaGetLastError();
     for (size_t i = 0; i < dst.size(); ++i)
         cuda_check(cudaMemcpyAsync(dst[i], src[i], sizes[i], cudaMemcpyDefault, st), "swap copy");
 }
