@@ -56,10 +56,12 @@ constexpr int kProdWarp = 4 * kSoftWG;
 constexpr int kMmaWarp = kProdWarp + 1;
 constexpr int kProdVWarp = kProdWarp + 2; // V tiles have their own producer: K(j+1) is never
                                           // queued behind a V stage that is still being read
+constexpr int kStoreWarp = kProdWarp + 3; // copies finished O tiles from shared memory to global
 constexpr int kTileRows = 128;        // M rows per query tile
 constexpr int kBN = 128;              // kv rows per kv tile (N of S = Q K^T, K of O += P V)
 #ifndef PB_K_STAGES
-#define PB_K_STAGES 3
+#define PB_K_STAGES 2 // 3 measured identical (the K tile of j+1 is always in before S(j+1)), so
+                      // its 32 KB hold the O staging tile instead
 #endif
 #ifndef PB_V_STAGES
 #define PB_V_STAGES 2
@@ -88,14 +90,24 @@ constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max gr
 #ifndef PB_ABLATE_MODE
 #define PB_ABLATE_MODE 0 // roofline ablations, separate builds only: 1 no softmax, 2 no exp2, 5 no P store
 #endif
-#ifndef PB_POLY_EVERY
-#define PB_POLY_EVERY 0 // one exp2 pair in N on the FMA pipe; 0 = all on MUFU
+#ifndef PB_POLY_COLS
+#define PB_POLY_COLS 0 // the last N columns of each S tile take exp2 on the FMA pipe (cubic)
+                       // before the MUFU share; measured slower at 32 and 64 (with or without
+                       // the lock) and at 1 pair in 2..4 interleaved
 #endif
+constexpr int kPolyCols = PB_POLY_COLS;
+static_assert(kPolyCols % 32 == 0 && kPolyCols <= 64, "poly columns: whole 32-column chunks of the second P half");
 #ifndef PB_P_HALVES
 #define PB_P_HALVES 1 // 1: P released in two 64-column halves, PV of the first half overlaps the
                       // softmax of the second
 #endif
 constexpr int kPParts = PB_P_HALVES ? 2 : 1;
+#ifndef PB_MUFU_LOCK
+#define PB_MUFU_LOCK 0 // 1: the two softmax warps of an SMSP (query tiles A, B) take turns on
+                       // the MUFU pipe.  Measured slower (434 vs 418 us on the config-4 tiles):
+                       // one warp alone cannot keep MUFU busy (the ex2 issue throttle stalls
+                       // it), so the exp2 phases do not get shorter, they only serialise
+#endif
 
 constexpr int kItemRing = 4; // work items fetched ahead by the TMA warp
 
@@ -105,10 +117,12 @@ constexpr int kItemRing = 4; // work items fetched ahead by the TMA warp
 #ifndef PB_TILE_TRACE
 #define PB_TILE_TRACE 0
 #endif
+// roles: 0/1 softmax A/B per tile, 2 MMA per kv tile, 3 K producer per item, 4 MMA per item,
+// 5 softmax A per item
 constexpr int kTraceCtas = 8, kTraceEvents = 1024, kTraceFields = 8;
 __device__ __forceinline__ unsigned long long* tile_trace_slot(unsigned long long* tr, int role, int ev) {
     if (!PB_TILE_TRACE || !tr || blockIdx.x >= kTraceCtas || ev >= kTraceEvents) return nullptr;
-    return tr + 148 * 2 * 4 + ((static_cast<size_t>(blockIdx.x) * 3 + role) * kTraceEvents + ev) * kTraceFields;
+    return tr + 148 * 2 * 4 + ((static_cast<size_t>(blockIdx.x) * 6 + role) * kTraceEvents + ev) * kTraceFields;
 }
 __device__ __forceinline__ unsigned long long clk64() {
     unsigned long long t;
@@ -122,6 +136,8 @@ struct __align__(1024) Smem {
     uint8_t q[2][kTileRows * D * 2];      // tiles A, B: [D/64][128 rows][128 B] K-major SW128
     uint8_t k[kKStages][kBN * D * 2];     // ring of kv tiles: [D/64][128 rows][128 B] K-major SW128
     uint8_t v[kVStages][kBN * D * 2];     // same layout, read as the MN-major SW128 B operand
+    uint8_t o[kTileRows * D * 2];         // finished O tile (bf16 rows, 16-B chunks XOR-swizzled)
+                                          // on its way to global through the store warp
     uint64_t q_full, q_empty;             // Q is released after the item's last S MMA
     uint64_t k_full[kKStages], k_empty[kKStages], v_full[kVStages], v_empty[kVStages];
     uint64_t s_full[2];                   // [query tile] S landed
@@ -131,6 +147,10 @@ struct __align__(1024) Smem {
     uint64_t item_full[kItemRing], item_empty[kItemRing];   // dynamic tile scheduler ring
     uint64_t drain;                       // MMA issuer: every commit of the pass has landed
     int32_t item_ring[kItemRing];
+    uint64_t o_full;                      // an O tile is staged (arrived by its group)
+    int32_t o_turn;                       // index of the next epilogue allowed to stage
+    int32_t o_info[2];                    // staged tile: first token row, first head
+    uint32_t mufu_lock[4];                // per SMSP: softmax warp using the MUFU pipe
 };
 
 // one CTA per SM: the larger of the two layouts plus 1 KiB of alignment slack must fit the
@@ -155,6 +175,10 @@ __device__ __forceinline__ ItemTiles item_tiles(const WorkItem& w, const SpanDev
     r.ntiles[1] = r.nt[1] > 0 ? ceil_div(sp.causal_offset + w.t0 + w.nt, kBN) : 0;
     r.n_kv = max(r.ntiles[0], r.ntiles[1]);
     return r;
+}
+
+__device__ __forceinline__ void named_bar_sync(int id, int count) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(count) : "memory");
 }
 
 // A operand in TMEM (P, bf16), B from shared memory (V).
@@ -188,15 +212,19 @@ __device__ __forceinline__ void tile_init(Smem<D>& s) { // thread 0
     }
     for (int i = 0; i < kItemRing; ++i) {
         mbar_init(&s.item_full[i], 1);
-        mbar_init(&s.item_empty[i], 2 + 4 * kSoftWG); // MMA thread, V producer + the softmax warps
+        mbar_init(&s.item_empty[i], 3 + 4 * kSoftWG); // MMA thread, V producer, store warp + the softmax warps
     }
     mbar_init(&s.drain, 1);
+    mbar_init(&s.o_full, 1);
+    s.o_turn = 0;
+    for (int i = 0; i < 4; ++i) s.mufu_lock[i] = 0;
 }
 template <int D>
 __device__ __forceinline__ void tile_inval(Smem<D>& s) { // thread 0, pipeline drained
     uint64_t* first = &s.q_full;
     uint64_t* last = &s.drain;
     for (uint64_t* b = first; b <= last; ++b) mbar_inval(b);
+    mbar_inval(&s.o_full);
 }
 
 // One launch for the whole ragged batch (BASELINE north star (a)): persistent CTAs, each
@@ -210,6 +238,7 @@ template <int D, int GD>
 __global__ void __launch_bounds__(kThreads, 1)
     attn_fused_sm100_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                             const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_qd,
+                            const __grid_constant__ CUtensorMap tm_o,
                             const AttnParams p) {
     constexpr int KH = D / 64;                  // 64-dim halves (one 128 B swizzle row each)
     constexpr uint32_t kHalfBytes = kTileRows * 128;   // one 64-dim half of a query tile
@@ -233,6 +262,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         tma_prefetch(&tm_k);
         tma_prefetch(&tm_v);
         tma_prefetch(&tm_qd);
+        tma_prefetch(&tm_o);
     }
     if (warp == kMmaWarp) tmem_alloc<kTmemCols>(&tmem_base_sh);
     tc_fence_before();
@@ -308,12 +338,16 @@ __global__ void __launch_bounds__(kThreads, 1)
                     item = *reinterpret_cast<volatile int32_t*>(&s.item_ring[slot]);
                     mbar_arrive(&s.item_empty[slot]);
                 }
+                unsigned long long* ti = kw ? tile_trace_slot(p.trace, 3, it) : nullptr;
+                if (ti) { ti[0] = clk64(); ti[7] = static_cast<unsigned long long>(item); }
                 if (item < 0) break;
                 const WorkItem w = p.items[item];
                 const SpanDev sp = p.spans[w.span];
                 const ItemTiles T = item_tiles(w, sp, tpt);
+                if (ti) ti[1] = clk64();
                 if (kw) {
                     if (it > 0) mbar_wait(&s.q_empty, (it - 1) & 1);
+                    if (ti) ti[2] = clk64();
                     mbar_arrive_expect_tx(&s.q_full, q_bytes * (T.nt[1] > 0 ? 2u : 1u));
                     for (int t = 0; t < 2; ++t)
                         if (T.nt[t] > 0)
@@ -343,7 +377,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                             for (int h = 0; h < KH; ++h)
                                 tma_load_3d(dst + h * kKvHalf + pg * chunk * 128, tm, full, h * 64, w.kvh, rows[pg]);
                     if (++st == n_st) { st = 0; ph ^= 1; }
+                    if (ti && j == 0) ti[3] = clk64();
                 }
+                if (ti) ti[4] = clk64();
             }
         }
     } else if (warp == kMmaWarp) {
@@ -367,10 +403,14 @@ __global__ void __launch_bounds__(kThreads, 1)
                     mbar_wait(&s.drain, 0);
                     break;
                 }
+                unsigned long long* ti = tile_trace_slot(p.trace, 4, it);
+                if (ti) { ti[0] = clk64(); ti[7] = static_cast<unsigned long long>(item); }
                 const WorkItem w = p.items[item];
                 const SpanDev sp = p.spans[w.span];
                 const ItemTiles T = item_tiles(w, sp, tpt);
+                if (ti) ti[1] = clk64();
                 mbar_wait(&s.q_full, it & 1);
+                if (ti) ti[2] = clk64();
                 tc_fence_after();
                 // S_t = Q_t K^T (K stage ks) into group t's S buffer.  Descriptors are advanced
                 // by adding (byte offset >> 4) to the start-address field (no carry: shared
@@ -389,8 +429,10 @@ __global__ void __launch_bounds__(kThreads, 1)
                 // prologue: S_A(0), S_B(0) from K(0)
                 mbar_wait(&s.k_full[kst], kph);
                 tc_fence_after();
+                if (ti) ti[3] = clk64();
                 for (int t = 0; t < 2; ++t)
                     if (T.ntiles[t] > 0) issue_s(t, kst);
+                if (ti) ti[4] = clk64();
                 umma_commit(&s.k_empty[kst]);
                 if (++kst == kKStages) { kst = 0; kph ^= 1; }
                 if (T.n_kv == 1) umma_commit(&s.q_empty); // Q is read by S MMAs only
@@ -443,6 +485,36 @@ __global__ void __launch_bounds__(kThreads, 1)
                 }
             }
         }
+    } else if (warp == kStoreWarp) {
+        // ============================ O store warp ==============================
+        // Full query tiles are staged one at a time in s.o (the SW128 layout of a TMA box
+        // {64 dims, g heads, 128/g tokens}), in an order every role can compute: per item,
+        // tile A then tile B, full tiles only.  For each: wait until it is staged, TMA-store
+        // it, wait until the bulk copy has read shared memory, hand the buffer to the next
+        // tile (o_turn).  The softmax groups never block on global stores.  Partial tiles
+        // (the last block of a span) are stored by their group directly.
+        if (elect_one()) {
+            int e = 0;
+            for (int it = 0;; ++it) {
+                const int slot = it % kItemRing;
+                mbar_wait(&s.item_full[slot], (it / kItemRing) & 1);
+                const int item = *reinterpret_cast<volatile int32_t*>(&s.item_ring[slot]);
+                mbar_arrive(&s.item_empty[slot]);
+                if (item < 0) break;
+                const int nt = p.items[item].nt;
+                const int n_epi = (nt >= tpt ? 1 : 0) + (nt == 2 * tpt ? 1 : 0);
+                for (int k = 0; k < n_epi; ++k, ++e) {
+                    mbar_wait(&s.o_full, e & 1);
+                    const int row0 = reinterpret_cast<volatile int32_t*>(s.o_info)[0];
+                    const int head0 = reinterpret_cast<volatile int32_t*>(s.o_info)[1];
+                    for (int h = 0; h < KH; ++h) tma_store_3d(&tm_o, s.o + h * kHalfBytes, h * 64, head0, row0);
+                    bulk_commit();
+                    bulk_wait_read0();
+                    *reinterpret_cast<volatile int32_t*>(&s.o_turn) = e + 1;
+                }
+            }
+            bulk_wait_all0(); // the pass's stores are complete before its smem is reused
+        }
     }
     mode_end(dec);
     }
@@ -471,6 +543,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         uint32_t n_o = 0;
         uint32_t c_t = 0;     // kv tiles processed by this group (s_full / p_full phase)
         uint32_t kv_seen = 0; // kv tiles loaded for earlier items (V ring position)
+        int epi = 0;          // epilogues (staged O tiles) of earlier items, both groups
         __nv_bfloat16* out = static_cast<__nv_bfloat16*>(p.out);
         for (int it = 0;; ++it) {
             const int slot = it % kItemRing;
@@ -478,13 +551,20 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int item = *reinterpret_cast<volatile int32_t*>(&s.item_ring[slot]);
             __syncwarp();
             if ((threadIdx.x & 31) == 0) mbar_arrive(&s.item_empty[slot]);
+            unsigned long long* ti = threadIdx.x == 0 ? tile_trace_slot(p.trace, 5, it) : nullptr;
+            if (ti) { ti[0] = clk64(); ti[7] = static_cast<unsigned long long>(item); }
             if (item < 0) break;
             const WorkItem w = p.items[item];
             const SpanDev sp = p.spans[w.span];
             const ItemTiles T = item_tiles(w, sp, tpt);
+            if (ti) ti[1] = clk64();
             const int n_tiles = T.ntiles[t];
             const uint32_t kv_base = kv_seen;
             kv_seen += static_cast<uint32_t>(T.n_kv);
+            // staged epilogues: full tiles only, A then B per item (the store warp's order)
+            const bool full_tile = T.nt[t] == tpt;
+            const int my_epi = epi + (t == 1 && T.nt[0] == tpt ? 1 : 0);
+            epi += (T.nt[0] == tpt ? 1 : 0) + (T.nt[1] == tpt ? 1 : 0);
             if (n_tiles == 0) continue;
             // rows of the span's last page past its context may hold anything (stale or
             // never-written pool memory): this group zeroes them in the V stage of the item's
@@ -563,7 +643,17 @@ __global__ void __launch_bounds__(kThreads, 1)
                 float2 ps[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) ps[u] = make_float2(0.f, 0.f);
-                const float2 sl2x2 = make_float2(sl2, sl2), negm = make_float2(-m_new, -m_new);
+                const float2 sl2x2 = make_float2(sl2, sl2);
+                // the FMA-pipe share first, outside the MUFU lock (results kept in x)
+#pragma unroll
+                for (int c = kBN - kPolyCols; c < kBN; c += 2) {
+                    const float2 e = exp2_neg_poly_x2(fma2(make_float2(x[c], x[c + 1]), sl2x2, make_float2(-m_new, -m_new)));
+                    ps[(c >> 1) & 3] = add2(ps[(c >> 1) & 3], e);
+                    x[c] = e.x;
+                    x[c + 1] = e.y;
+                }
+                const float m_arg = PB_MUFU_LOCK ? m_new + __uint_as_float(smsp_lock_acquire(&s.mufu_lock[quad])) : m_new;
+                const float2 negm = make_float2(-m_arg, -m_arg);
 #pragma unroll
                 for (int h = 0; h < kPParts; ++h) {
 #pragma unroll
@@ -571,19 +661,20 @@ __global__ void __launch_bounds__(kThreads, 1)
                         uint32_t pk[16];
 #pragma unroll
                         for (int c = c0; c < c0 + 32; c += 2) {
-                            // exp2((s - max) * log2e / scale) on packed pairs (FFMA2 / FADD2) and MUFU
-                            const float2 a = fma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
                             float2 e;
-                            if (ablate == 2) { // profiling: no exponentials
-                                e = a;
-                            } else if (PB_POLY_EVERY > 0 &&
-                                       ((c >> 1) % (PB_POLY_EVERY > 0 ? PB_POLY_EVERY : 1)) == PB_POLY_EVERY - 1) {
-                                e = exp2_neg_poly_x2(a);
+                            if (c >= kBN - kPolyCols) { // done on the FMA pipe above
+                                e = make_float2(x[c], x[c + 1]);
                             } else {
-                                e.x = ex2(a.x);
-                                e.y = ex2(a.y);
+                                // exp2((s - max) * log2e / scale) on packed pairs (FFMA2 / FADD2) and MUFU
+                                const float2 a = fma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
+                                if (ablate == 2) { // profiling: no exponentials
+                                    e = a;
+                                } else {
+                                    e.x = ex2(a.x);
+                                    e.y = ex2(a.y);
+                                }
+                                ps[(c >> 1) & 3] = add2(ps[(c >> 1) & 3], e);
                             }
-                            ps[(c >> 1) & 3] = add2(ps[(c >> 1) & 3], e);
                             pk[(c - c0) >> 1] = pack_bf16x2(e.x, e.y);
                         }
                         // P (bf16) over the first 64 columns of this S buffer (all of S is in
@@ -594,6 +685,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     tc_fence_before();
                     mbar_arrive(&s.p_full[t][h]);
                 }
+                if (PB_MUFU_LOCK) smsp_lock_release(&s.mufu_lock[quad]);
                 if (tt) {
                     tt[3] = clk64();
                     tt[4] = clk64();
@@ -607,31 +699,57 @@ __global__ void __launch_bounds__(kThreads, 1)
                 m_run = m_new;
             }
             // epilogue: O / l -> bf16 -> global
+            if (ti) ti[2] = clk64();
             mbar_wait(&s.o_ready[t], n_o & 1);
+            if (ti) ti[3] = clk64();
             ++n_o;
             tc_fence_after();
             const float inv_l = 1.f / l_run;
-            const int h = w.kvh * g + (row % g);
-            __nv_bfloat16* orow = out + (static_cast<size_t>(sp.query_start + tok0 + t_local) * p.n_head + h) * D;
+            // the whole row into registers (all TMEM loads in flight at once), bf16 16-B
+            // chunks, so O_t is released to the next item's PV before anything is stored
+            uint4 chv[D / 8];
+            {
+                uint32_t o[D];
 #pragma unroll
-            for (int c = 0; c < D / 32; ++c) {
-                uint32_t o[32];
-                tmem_ld32(t_lane + col_o + c * 32, o);
+                for (int c = 0; c < D / 32; ++c)
+                    tmem_ld32(t_lane + col_o + c * 32, *reinterpret_cast<uint32_t(*)[32]>(&o[c * 32]));
                 tmem_ld_wait();
-                if (valid) {
 #pragma unroll
-                    for (int e = 0; e < 32; e += 8) {
-                        uint4 v;
-                        v.x = pack_bf16x2(__uint_as_float(o[e + 0]) * inv_l, __uint_as_float(o[e + 1]) * inv_l);
-                        v.y = pack_bf16x2(__uint_as_float(o[e + 2]) * inv_l, __uint_as_float(o[e + 3]) * inv_l);
-                        v.z = pack_bf16x2(__uint_as_float(o[e + 4]) * inv_l, __uint_as_float(o[e + 5]) * inv_l);
-                        v.w = pack_bf16x2(__uint_as_float(o[e + 6]) * inv_l, __uint_as_float(o[e + 7]) * inv_l);
-                        *reinterpret_cast<uint4*>(orow + c * 32 + e) = v;
-                    }
+                for (int c = 0; c < D / 8; ++c) {
+                    const uint32_t* q8 = o + c * 8;
+                    chv[c] = make_uint4(
+                        pack_bf16x2(__uint_as_float(q8[0]) * inv_l, __uint_as_float(q8[1]) * inv_l),
+                        pack_bf16x2(__uint_as_float(q8[2]) * inv_l, __uint_as_float(q8[3]) * inv_l),
+                        pack_bf16x2(__uint_as_float(q8[4]) * inv_l, __uint_as_float(q8[5]) * inv_l),
+                        pack_bf16x2(__uint_as_float(q8[6]) * inv_l, __uint_as_float(q8[7]) * inv_l));
                 }
             }
             tc_fence_before();
             mbar_arrive(&s.o_empty[t]);
+            if (ti) ti[5] = clk64();
+            if (full_tile) {
+                // stage the row for the store warp once the buffer is this tile's turn
+                if (threadIdx.x % 128 == 0)
+                    while (*reinterpret_cast<volatile int32_t*>(&s.o_turn) != my_epi) __nanosleep(32);
+                named_bar_sync(2 + t, 128);
+                if (ti) ti[6] = clk64();
+#pragma unroll
+                for (int c = 0; c < D / 8; ++c)
+                    *reinterpret_cast<uint4*>(s.o + (c >> 3) * kHalfBytes + row * 128 + (((c & 7) ^ (row & 7)) << 4)) = chv[c];
+                fence_proxy_async_smem(); // generic-proxy writes -> the TMA (async proxy) read
+                if (threadIdx.x % 128 == 0) {
+                    s.o_info[0] = sp.query_start + tok0;
+                    s.o_info[1] = w.kvh * g;
+                }
+                named_bar_sync(2 + t, 128);
+                if (threadIdx.x % 128 == 0) mbar_arrive(&s.o_full);
+            } else if (valid) {
+                __nv_bfloat16* orow =
+                    out + (static_cast<size_t>(sp.query_start + tok0 + t_local) * p.n_head + w.kvh * g + (row % g)) * D;
+#pragma unroll
+                for (int c = 0; c < D / 8; ++c) *reinterpret_cast<uint4*>(orow + c * 8) = chv[c];
+            }
+            if (ti) ti[4] = clk64();
         }
     }
     mode_end(dec);
@@ -690,7 +808,7 @@ void launch_fused(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st)
     set_smem_once(attr, attn_fused_sm100_kernel<D, GD>, smem, "cudaFuncSetAttribute(fused smem)");
     const int grid = std::min(p.n_items + (D == 128 ? p.n_dec_items : 0), device_sms());
     if (!p.k_new) {
-        attn_fused_sm100_kernel<D, GD><<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], p);
+        attn_fused_sm100_kernel<D, GD><<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], p);
         cuda_check(cudaGetLastError(), "attn_fused_sm100 launch");
         count_launch();
         return;
@@ -709,7 +827,7 @@ void launch_fused(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st)
     attr_coop.val.cooperative = 1;
     cfg.attrs = &attr_coop;
     cfg.numAttrs = 1;
-    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_fused_sm100_kernel<D, GD>, maps[0], maps[1], maps[2], maps[3], p);
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, attn_fused_sm100_kernel<D, GD>, maps[0], maps[1], maps[2], maps[3], maps[4], p);
     if (e == cudaSuccess) {
         count_launch();
         return;
@@ -720,7 +838,7 @@ void launch_fused(const AttnParams& p, const CUtensorMap* maps, cudaStream_t st)
     AttnParams q = p;
     q.k_new = nullptr;
     q.v_new = nullptr;
-    attn_fused_sm100_kernel<D, GD><<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], q);
+    attn_fused_sm100_kernel<D, GD><<<grid, kThreads, smem, st>>>(maps[0], maps[1], maps[2], maps[3], maps[4], q);
     cuda_check(cudaGetLastError(), "attn_fused_sm100 launch");
     count_launch();
 }
@@ -737,7 +855,7 @@ int sm100_tile_tokens(int group) { return 2 * (kTileRows / group); } // two quer
 void sm100_prepare_maps(const AttnParams& p, const pb_attn_shape& shape, Sm100Cache& cache, int64_t total_tokens) {
     const int D = shape.head_size;
     const int g = shape.n_head / shape.n_kv_head;
-    if (!cache.valid || cache.q != p.q || cache.k != p.k_pages || cache.v != p.v_pages ||
+    if (!cache.valid || cache.q != p.q || cache.k != p.k_pages || cache.v != p.v_pages || cache.out != p.out ||
         cache.total_tokens != total_tokens) {
         auto* m = reinterpret_cast<CUtensorMap*>(cache.maps);
         encode_3d(&m[0], p.q, D, shape.n_head, std::max<int64_t>(total_tokens, 1), D * 2ull,
@@ -750,9 +868,13 @@ void sm100_prepare_maps(const AttnParams& p, const pb_attn_shape& shape, Sm100Ca
         // decode rows: the g query heads of one kv head for one token
         encode_3d(&m[3], p.q, D, shape.n_head, std::max<int64_t>(total_tokens, 1), D * 2ull,
                   static_cast<uint64_t>(shape.n_head) * D * 2, 64, g, 1);
+        // output tiles (TMA store of a staged full query tile): the q tile geometry over out
+        encode_3d(&m[4], p.out, D, shape.n_head, std::max<int64_t>(total_tokens, 1), D * 2ull,
+                  static_cast<uint64_t>(shape.n_head) * D * 2, 64, g, kTileRows / g);
         cache.q = p.q;
         cache.k = p.k_pages;
         cache.v = p.v_pages;
+        cache.out = p.out;
         cache.total_tokens = total_tokens;
         cache.valid = true;
     }

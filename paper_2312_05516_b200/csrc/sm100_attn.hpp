@@ -16,8 +16,9 @@ struct Sm100Cache {
     const void* q = nullptr;
     const void* k = nullptr;
     const void* v = nullptr;
+    const void* out = nullptr;
     int64_t total_tokens = -1;
-    alignas(64) unsigned char maps[4][128]; // q tiles, k pages, v pages, q decode rows
+    alignas(64) unsigned char maps[5][128]; // q tiles, k pages, v pages, q decode rows, out tiles
     bool valid = false;
 };
 

@@ -65,6 +65,24 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
 #endif
 }
 
+// A per-SM-sub-partition lock held by one warp across its run of MUFU ex2 instructions, so
+// two softmax warps on one SMSP take the MUFU pipe in turn instead of sharing it (each tile's
+// exponentials finish in half the time and its P reaches the tensor pipe earlier).
+// acquire returns the winning compare-and-swap's old value (always 0) broadcast to the warp:
+// the caller folds it into the exp2 arguments, a data dependency that keeps ptxas from
+// scheduling the exponentials above the lock.  Release after the P barrier arrive (a shared
+// memory operation behind the tcgen05.st wait, so after every ex2 it depends on).
+__device__ __forceinline__ uint32_t smsp_lock_acquire(uint32_t* lk) {
+    uint32_t old = 0;
+    if ((threadIdx.x & 31) == 0)
+        while ((old = atomicCAS(lk, 0u, 1u)) != 0u) __nanosleep(16);
+    return __shfl_sync(0xffffffffu, old, 0);
+}
+__device__ __forceinline__ void smsp_lock_release(uint32_t* lk) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) atomicExch(lk, 0u);
+}
+
 // ---------------------------------------------------------------- fences
 __device__ __forceinline__ void fence_proxy_async_smem() {
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -88,6 +106,19 @@ __device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, u
         "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2)
         : "memory");
 }
+
+// shared -> global TMA store of one box (bulk-group completion)
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* src, int c0, int c1, int c2) {
+    asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(map)),
+                 "r"(smem_u32(src)), "r"(c0), "r"(c1), "r"(c2)
+                 : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+// the committed bulk stores have finished reading shared memory (the buffer may be rewritten)
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+// the committed bulk stores are complete (writes performed)
+__device__ __forceinline__ void bulk_wait_all0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 
 // ---------------------------------------------------------------- TMEM
 template <uint32_t kCols>

@@ -29,14 +29,14 @@ stream = torch.cuda.current_stream().cuda_stream
 plan.upload(stream)
 out = torch.empty_like(q)
 ws = torch.zeros(max(1, plan.workspace_bytes()), dtype=torch.uint8, device="cuda")
-n = 148 * 2 * 4 + 8 * 3 * 1024 * 8
+n = 148 * 2 * 4 + 8 * 6 * 1024 * 8
 tr = torch.zeros(n, dtype=torch.int64, device="cuda")
 for i in range(4):
     if i == 3:
         plan.set_trace(tr.data_ptr())
     plan.run(q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr(), ws.data_ptr(), stream)
 torch.cuda.synchronize()
-t = tr.cpu().numpy()[148 * 2 * 4:].reshape(8, 3, 1024, 8)
+t = tr.cpu().numpy()[148 * 2 * 4:].reshape(8, 6, 1024, 8)
 res = {}
 for role, name in ((0, "softmax_A"), (1, "softmax_B")):
     d = {"wait_S": [], "ld_max": [], "exp": [], "st_arrive": [], "period": []}
@@ -75,4 +75,26 @@ res["cta0_A_first"] = [[int(x - base) for x in e[:5]] + [int(e[5]), int(e[6]), i
 ev = t[0, 2]
 ev = ev[ev[:, 0] > 0][:40]
 res["cta0_mma_first"] = [[int(x - base) if x else 0 for x in e[:6]] + [int(e[6]), int(e[7])] for e in ev]
+# item boundaries (CTA 0..7): K producer {ticket, item read, q_empty passed, K(0) issued, last
+# K issued}; MMA {item read, q_full, k_full(0), S(0) issued}; softmax A {item read, last tile
+# done, o_ready, epilogue done}
+for role, name, fields in ((3, "prod_item", ["read", "q_empty", "k0_issued", "all_k_issued"]),
+                           (4, "mma_item", ["read", "q_full", "k0_full", "s0_issued"]),
+                           (5, "softA_item", ["read", "tiles", "o_ready", "tmem_out", "store_half0", "store_half1"])):
+    d = {f: [] for f in fields}
+    for c in range(8):
+        ev = t[c, role]
+        ev = ev[ev[:, 0] > 0]
+        for e in ev:
+            if int(e[7]) < 0:
+                continue
+            seq = [0, 1, 2, 3, 5, 6, 4] if role == 5 else list(range(len(fields) + 1))
+            for i, f in enumerate(fields):
+                a, b = seq[i], seq[i + 1]
+                if e[b] and e[a]:
+                    d[f].append(int(e[b]) - int(e[a]))
+    res[name] = {f: int(statistics.median(v)) for f, v in d.items() if v}
+    ev = t[0, role]
+    ev = ev[ev[:, 0] > 0][:6]
+    res[name + "_cta0"] = [[int(x - base) if x else 0 for x in e[:7]] + [int(e[7])] for e in ev]
 print(json.dumps(res))
