@@ -22,9 +22,14 @@ from paper_2312_05516_b200.abi import AttentionPlan, PB_PLAN_SEPARATE_DECODE  # 
 from paper_2312_05516_b200.workloads import config  # noqa: E402
 
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+world = int(sys.argv[2]) if len(sys.argv) > 2 else 1  # rank 0 of an N-way kv-head shard
 w = config(cfg)
+if world > 1:
+    from paper_2312_05516_b200.sharding import shard_shape  # noqa: E402
+    _sh = shard_shape(w.shape(), 0, world)
+    w.n_kv_head, w.n_head = _sh.n_kv_head, _sh.n_head
 q, k, v = gh.device_inputs(w)
-plan = AttentionPlan(w.shape(), w.batch(), PB_PLAN_SEPARATE_DECODE)
+plan = AttentionPlan(_sh if world > 1 else w.shape(), w.batch(), PB_PLAN_SEPARATE_DECODE)
 stream = torch.cuda.current_stream().cuda_stream
 plan.upload(stream)
 out = torch.empty_like(q)
@@ -97,4 +102,16 @@ for role, name, fields in ((3, "prod_item", ["read", "q_empty", "k0_issued", "al
     ev = t[0, role]
     ev = ev[ev[:, 0] > 0][:6]
     res[name + "_cta0"] = [[int(x - base) if x else 0 for x in e[:7]] + [int(e[7])] for e in ev]
+# per-CTA item timeline (softmax A, first 8 CTAs, us at 1.9 GHz): item, start, tiles done, epilogue done
+tl = {}
+for c in range(8):
+    ev = t[c, 5]
+    ev = ev[ev[:, 0] > 0]
+    b0 = t[c, 0][t[c, 0][:, 0] > 0]
+    if len(b0) == 0:
+        continue
+    z = int(b0[0, 0])
+    tl[c] = [[int(e[7]), round((int(e[1]) - z) / 1900, 1), round((int(e[2]) - z) / 1900, 1),
+              round((int(e[4]) - z) / 1900, 1)] for e in ev if int(e[7]) >= 0]
+res["timeline"] = tl
 print(json.dumps(res))
