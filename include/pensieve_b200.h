@@ -79,7 +79,10 @@ enum {
     PB_PLAN_SINGLE_TOKEN = 1, /* single_token_attention contract: every query_len == 1 */
     PB_PLAN_FORCE_SIMT = 2,   /* route every span through the SIMT kernel (diagnostics) */
     PB_PLAN_NO_SPLIT = 4,     /* never split a decode span's context across CTAs */
-    PB_PLAN_SEPARATE_DECODE = 8 /* decode units in their own launch instead of the fused one */
+    PB_PLAN_SEPARATE_DECODE = 8, /* decode units in their own launch instead of the fused one */
+    PB_PLAN_LPT_ORDER = 16       /* tile queue in strict LPT order (default: LPT below 8 items per
+                                    SM, else grouped by span and kv head for L2 reuse); changes
+                                    timing only, never the outputs */
 };
 
 /* Validates the batch exactly as check_batch (src/attention.cpp:23-48, minus the q

@@ -22,6 +22,7 @@ PB_PLAN_SINGLE_TOKEN = 1
 PB_PLAN_FORCE_SIMT = 2
 PB_PLAN_NO_SPLIT = 4
 PB_PLAN_SEPARATE_DECODE = 8
+PB_PLAN_LPT_ORDER = 16
 
 
 class PBError(RuntimeError):

@@ -18,6 +18,10 @@
 #include <string>
 #include <vector>
 
+#ifndef PB_DEC_CTA_SCALE_SMALL
+#define PB_DEC_CTA_SCALE_SMALL 2.0 // decode CTA share multiplier below a 25% decode share
+#endif
+
 namespace pb {
 void launch_attn_simt(const AttnParams& p, int dtype, int n_items, cudaStream_t stream);
 void launch_check_numerics(const AttnParams& p, int dtype, int64_t q_elems, int32_t* d_flag,
@@ -140,8 +144,17 @@ void build_work(pb_attn_plan& P) {
     // per CTA (cfg3: 95% -> 99% of HBM; the config-5 steps: 52 -> 40 us); with fewer pairs,
     // split to ~1.5 units per CTA (>= 16 pages each).
     const int64_t sms = sm_count();
+    bool multi_token = false;
+    for (const SpanDev& sp : P.spans) multi_token = multi_token || sp.query_len >= 2;
+    // In the fused launch the tile items fill the SMs, so decode spans stay whole: splitting
+    // them to fill the GPU (the decode-only rule below) only adds partial writes and merges
+    // to the few decode CTAs (config 4 at an 8-way shard: 86.0 -> 75.8 us per layer, 4-way
+    // 136.7 -> 126.5; unchanged at 1- and 2-way, where nothing is split).
+    const bool fused_launch = dec_tc && tc && multi_token && !(P.flags & PB_PLAN_SEPARATE_DECODE);
     int split_pages;
-    if (dec_tc)
+    if (dec_tc && fused_launch)
+        split_pages = 1 << 24; // no split
+    else if (dec_tc)
         split_pages = decode_pairs >= sms
                           ? (1 << 24) // no split
                           : static_cast<int>(std::max<int64_t>(16, (2 * decode_pages + 3 * sms - 1) / (3 * sms)));
@@ -172,9 +185,10 @@ void build_work(pb_attn_plan& P) {
                     w.nt = std::min(tc_tokens, sp.query_len - t0);
                     w.group = -1;
                     const double kv = sp.causal_offset + w.t0 + w.nt;
-                    // est. SM cycles: a 128-position kv tile is ~3400 cycles for two
-                    // query tiles at the measured MMA/softmax rate
-                    tc_list.push_back({kv * (w.nt > sm100_tile_tokens(g) / 2 ? 26.5 : 13.3), w});
+                    // est. SM cycles per kv position: a 128-position kv tile takes ~3400
+                    // cycles for two query tiles and ~3000 for one (tile trace: one softmax
+                    // group alone is latency-bound, not half the work)
+                    tc_list.push_back({kv * (w.nt > sm100_tile_tokens(g) / 2 ? 26.5 : 23.5), w});
                     ++P.n_prefill;
                 }
             } else if (!P.decode_kernel) {
@@ -229,7 +243,13 @@ void build_work(pb_attn_plan& P) {
         std::stable_sort(v.begin(), v.end(), [](const auto& a, const auto& b) { return a.first > b.first; });
     };
     lpt(dec_list);
-    if (!tc_list.empty()) {
+    // Few items per CTA (small shards, e.g. config 4 at a 2..8-way kv-head shard): strict LPT,
+    // so no heavy item is taken late by a CTA that already ran one (per-CTA end times: N = 8
+    // max 57.4 vs 59.3 us grouped, N = 2 195.3 vs 198.9).  Many items per CTA: grouped by
+    // (span, kv head) for L2 reuse of the shared K/V pages (N = 1: 372.4 vs 377.3 us).
+    if (!tc_list.empty() && ((P.flags & PB_PLAN_LPT_ORDER) || static_cast<int64_t>(tc_list.size()) < 8 * sms)) {
+        lpt(tc_list);
+    } else if (!tc_list.empty()) {
         // The query blocks of one (span, kv head) stream the same K/V pages: keeping them
         // adjacent in the queue lets concurrently running CTAs share those pages through L2.
         // Groups go heaviest first (by their heaviest item), items heaviest first inside.
@@ -470,7 +490,7 @@ static void run_impl(pb_attn_plan* P, const void* q, const void* k_pages, const 
             // small decode share is under-estimated: double it below 25% (measured: cfg4 at an
             // 8-way kv-head shard 92 -> 83 us per layer, unchanged at N = 1; cfg2, where decode
             // is most of the launch, is best unscaled, profiles/r1_variants.md).
-            const double cta_scale = P->dec_share < 0.25 ? 2.0 : 1.0;
+            const double cta_scale = P->dec_share < 0.25 ? PB_DEC_CTA_SCALE_SMALL : 1.0;
             AttnParams pf = p;
             pf.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_tc);
             pf.n_items = static_cast<int32_t>(P->tc_items.size());

@@ -256,6 +256,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int ppt = kBN / chunk;           // pages per kv tile
     int* ctr = p.work_counter;             // [2] next tile item, [3] retired CTAs, [4] next decode unit
 
+    if (threadIdx.x == 0 && p.trace) { // CTA entry (pass-0 record, field 1)
+        unsigned long long t;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+        p.trace[static_cast<size_t>(blockIdx.x) * 8 + 1] = t;
+    }
     append_prologue(p, ctr); // fused K/V append, when the launch carries new rows
     if (threadIdx.x == 0) {
         tma_prefetch(&tm_q);
@@ -767,6 +772,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     if (warp == kMmaWarp) {
         tc_fence_after();
         tmem_dealloc<kTmemCols>(tmem);
+        if (p.trace && (threadIdx.x & 31) == 0) { // CTA exit (pass-1 record, field 1)
+            unsigned long long t;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+            p.trace[static_cast<size_t>(blockIdx.x) * 8 + 4 + 1] = t;
+        }
     }
 }
 

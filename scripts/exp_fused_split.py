@@ -18,7 +18,7 @@ sys.path.insert(0, os.path.join(ROOT, "tests"))
 import torch  # noqa: E402
 
 import gpu_helpers as gh  # noqa: E402
-from paper_2312_05516_b200.abi import PB_PLAN_SEPARATE_DECODE, AttentionPlan  # noqa: E402
+from paper_2312_05516_b200.abi import PB_PLAN_NO_SPLIT, PB_PLAN_SEPARATE_DECODE, AttentionPlan  # noqa: E402
 from paper_2312_05516_b200.sharding import shard_shape  # noqa: E402
 from paper_2312_05516_b200.workloads import PB_BF16, SplitMix64, _build, config  # noqa: E402
 
@@ -61,6 +61,7 @@ mk = lambda name, cv: _build(name, base.n_head, base.n_kv_head, base.head_size, 
 res = {"config": cfg, "world": world,
        "fused": timed(mk("all", convs)),
        "separate": timed(mk("all", convs), PB_PLAN_SEPARATE_DECODE),
+       "fused_no_split": timed(mk("all", convs), PB_PLAN_NO_SPLIT),
        "tiles_only": timed(mk("pre", pre)),
        "decode_only": timed(mk("dec", dec))}
 print(json.dumps(res))
