@@ -21,6 +21,10 @@
 #ifndef PB_DEC_CTA_SCALE_SMALL
 #define PB_DEC_CTA_SCALE_SMALL 2.0 // decode CTA share multiplier below a 25% decode share
 #endif
+#ifndef PB_DEC_CTA_SCALE_LARGE
+#define PB_DEC_CTA_SCALE_LARGE 0.6 // ... and at or above it (config 2: 5014 -> 5104 GB/s, config 5:
+                                   // 3939 -> 4053 over 1.0; 0.4-1.2 swept, profiles/r2_experiments.md)
+#endif
 
 namespace pb {
 void launch_attn_simt(const AttnParams& p, int dtype, int n_items, cudaStream_t stream);
@@ -490,7 +494,7 @@ static void run_impl(pb_attn_plan* P, const void* q, const void* k_pages, const 
             // small decode share is under-estimated: double it below 25% (measured: cfg4 at an
             // 8-way kv-head shard 92 -> 83 us per layer, unchanged at N = 1; cfg2, where decode
             // is most of the launch, is best unscaled, profiles/r1_variants.md).
-            const double cta_scale = P->dec_share < 0.25 ? PB_DEC_CTA_SCALE_SMALL : 1.0;
+            const double cta_scale = P->dec_share < 0.25 ? PB_DEC_CTA_SCALE_SMALL : PB_DEC_CTA_SCALE_LARGE;
             AttnParams pf = p;
             pf.items = reinterpret_cast<const WorkItem*>(static_cast<uint8_t*>(P->d_buf) + P->off_tc);
             pf.n_items = static_cast<int32_t>(P->tc_items.size());
