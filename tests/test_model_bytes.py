@@ -90,3 +90,20 @@ def test_exported():
     for n in ("pb_model_validate", "pb_model_kv_token_bytes", "pb_model_chunk_bytes", "pb_model_preset",
               "pb_shard_shape", "pb_tier_set_policy"):
         assert n in abi.exported_symbols()
+
+
+def test_reference_model_config_unit_tests_pass_on_pb_model():
+    """The reference's OWN ModelConfig unit tests (proj/tests/test_model_config.cpp, 7 cases,
+    compiled unchanged) with ModelConfig::validate / kv_token_bytes / chunk_bytes / preset
+    resolved to this library's pb_model_* at link time (oracle/ref_tests_b200_model.cpp,
+    oracle/Makefile).  Host code only."""
+    import os
+    import subprocess
+
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "..", "oracle", "_ref",
+                       "kvsim_model_config_tests_b200")
+    if not os.path.exists(exe) or not os.path.isdir("/root/reference/proj/data"):
+        pytest.skip("needs the reference build and its data directory (this container only)")
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "test cases: 7 | 7 passed | 0 failed" in r.stdout, r.stdout
