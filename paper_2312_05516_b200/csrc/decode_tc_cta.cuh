@@ -60,7 +60,10 @@ struct __align__(1024) DtSmem {
     // has read it, so K runs further ahead and more bytes are in flight per CTA
     uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
     uint64_t q_full[2], q_empty[2];
-    uint64_t s_full[2], p_full, pv_done, o_empty;
+    // p_full / pv_done per tile parity: the softmax may run one tile ahead of the MMA warp's
+    // p_full wait (it no longer waits for PV(j-1) before releasing P(j)), so a single barrier
+    // could be lapped; per parity every wait is at most one phase behind
+    uint64_t s_full[2], p_full[2], pv_done[2], o_empty;
     uint64_t item_full[kRing], item_empty[kRing];
     uint64_t drain;                 // MMA issuer: every commit of the pass has landed
     int32_t item_ring[kRing];
@@ -68,6 +71,13 @@ struct __align__(1024) DtSmem {
 };
 
 __device__ __forceinline__ void bar_softmax() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
+// max over the warp in one instruction (sm_100a redux.sync on f32)
+__device__ __forceinline__ float warp_max_f32(float v) {
+    float r;
+    asm volatile("redux.sync.max.f32 %0, %1, 0xffffffff;" : "=f"(r) : "f"(v));
+    return r;
+}
 
 __device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&r)[16]) {
     asm volatile(
@@ -110,8 +120,10 @@ __device__ __forceinline__ void decode_cta_init(DtSmem& s) {
         mbar_init(&s.q_empty[i], 1);
         mbar_init(&s.s_full[i], 1);
     }
-    mbar_init(&s.p_full, 128);
-    mbar_init(&s.pv_done, 1);
+    for (int i = 0; i < 2; ++i) {
+        mbar_init(&s.p_full[i], 128);
+        mbar_init(&s.pv_done[i], 1);
+    }
     mbar_init(&s.o_empty, 128);
     for (int i = 0; i < kRing; ++i) {
         mbar_init(&s.item_full[i], 1);
@@ -133,8 +145,10 @@ __device__ __forceinline__ void decode_cta_inval(DtSmem& s) {
         mbar_inval(&s.q_empty[i]);
         mbar_inval(&s.s_full[i]);
     }
-    mbar_inval(&s.p_full);
-    mbar_inval(&s.pv_done);
+    for (int i = 0; i < 2; ++i) {
+        mbar_inval(&s.p_full[i]);
+        mbar_inval(&s.pv_done[i]);
+    }
     mbar_inval(&s.o_empty);
     for (int i = 0; i < kRing; ++i) {
         mbar_inval(&s.item_full[i]);
@@ -283,7 +297,7 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                         tc_fence_after();
                         issue_s(qb, T + 1);
                     }
-                    mbar_wait(&s.p_full, T & 1);
+                    mbar_wait(&s.p_full[T & 1], (T >> 1) & 1);
                     if (j == 0 && it > 0) mbar_wait(&s.o_empty, (it - 1) & 1);
                     mbar_wait(&s.v_full[vstage], vph);
                     tc_fence_after();
@@ -294,7 +308,7 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                         const uint32_t ob = ((kk >> 2) * (kN * 128) + (kk & 3) * 32) >> 4;
                         umma_bf16_ss(tmem + kColO, ad + kk * (2048 >> 4), bd + ob, idesc_o, (j > 0 || kk > 0) ? 1u : 0u);
                     }
-                    umma_commit(&s.pv_done);
+                    umma_commit(&s.pv_done[T & 1]);
                     umma_commit(&s.v_empty[vstage]);
                     if (++vstage == kStages) { vstage = 0; vph ^= 1; }
                 }
@@ -340,10 +354,7 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
                     x[h] = (valid && h < g) ? __uint_as_float(sr[h]) * sl2 : -CUDART_INF_F;
-                    float m = x[h];
-#pragma unroll
-                    for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
-                    mt[h] = m;
+                    mt[h] = warp_max_f32(x[h]);
                 }
                 if (lane < G) {
                     float v = mt[0];
@@ -386,9 +397,13 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
 #pragma unroll
                         for (int c = 0; c < 8; ++c) st_shared_zero16(smem_u32(s.v[stg][h]) + r * 128 + c * 16);
                 }
-                if (j > 0) {
-                    mbar_wait(&s.pv_done, (T - 1) & 1); // PV(j-1) complete: O may be rescaled
-                    if (rescale) {
+                if (rescale) {
+                    // O may be rescaled once PV(j-1) is complete.  S(j) landing already proves
+                    // PV(j-2) complete (S(j) is issued after it), so this parity wait is exact;
+                    // without a rescale nothing waits for PV(j-1) (P^T is double-buffered and
+                    // its buffer's previous reader, PV(j-2), is done)
+                    mbar_wait(&s.pv_done[(T - 1) & 1], ((T - 1) >> 1) & 1);
+                    {
                         tc_fence_after();
                         uint32_t o[16];
                         tmem_ld16(t_lane + kColO, o);
@@ -401,10 +416,10 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                 }
                 fence_proxy_async_smem();
                 tc_fence_before();
-                mbar_arrive(&s.p_full);
+                mbar_arrive(&s.p_full[T & 1]);
             }
             // ---------------- epilogue: O^T lane r = output dim r ----------------
-            mbar_wait(&s.pv_done, (T - 1) & 1);
+            mbar_wait(&s.pv_done[(T - 1) & 1], ((T - 1) >> 1) & 1);
             tc_fence_after();
             uint32_t o[16];
             tmem_ld16(t_lane + kColO, o);

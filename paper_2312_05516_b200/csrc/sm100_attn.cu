@@ -96,6 +96,9 @@ constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max gr
                        // the lock) and at 1 pair in 2..4 interleaved
 #endif
 constexpr int kPolyCols = PB_POLY_COLS;
+#ifndef PB_POLY_EVERY
+#define PB_POLY_EVERY 0 // exp2 of one pair in N on the FMA pipe, interleaved with the MUFU pairs
+#endif
 static_assert(kPolyCols % 32 == 0 && kPolyCols <= 64, "poly columns: whole 32-column chunks of the second P half");
 #ifndef PB_P_HALVES
 #define PB_P_HALVES 1 // 1: P released in two 64-column halves, PV of the first half overlaps the
@@ -674,6 +677,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                                 const float2 a = fma2(make_float2(x[c], x[c + 1]), sl2x2, negm);
                                 if (ablate == 2) { // profiling: no exponentials
                                     e = a;
+                                } else if (PB_POLY_EVERY > 0 && ((c >> 1) % (PB_POLY_EVERY > 0 ? PB_POLY_EVERY : 1)) == 0) {
+                                    e = exp2_neg_poly_x2(a);
                                 } else {
                                     e.x = ex2(a.x);
                                     e.y = ex2(a.y);
