@@ -72,6 +72,22 @@ struct __align__(1024) DtSmem {
 
 __device__ __forceinline__ void bar_softmax() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
 
+#ifndef PB_TILE_TRACE
+#define PB_TILE_TRACE 0
+#endif
+// Diagnostics build only (-DPB_TILE_TRACE=1): per-tile clock64 stamps of the first 8 CTAs, in
+// the layout of sm100_attn.cu's tile trace (roles: 0 softmax, 2 MMA, 3 K producer, 4 V
+// producer); scripts/trace_decode.py reads them.  Compiles to nothing by default.
+__device__ __forceinline__ unsigned long long* dt_trace_slot(unsigned long long* tr, int role, uint32_t ev) {
+    if (!PB_TILE_TRACE || !tr || blockIdx.x >= 8 || ev >= 1024) return nullptr;
+    return tr + 148 * 2 * 4 + ((static_cast<size_t>(blockIdx.x) * 6 + role) * 1024 + ev) * 8;
+}
+__device__ __forceinline__ unsigned long long dt_clk() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    return t;
+}
+
 // max over the warp in one instruction (sm_100a redux.sync on f32)
 __device__ __forceinline__ float warp_max_f32(float v) {
     float r;
@@ -179,6 +195,7 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
             uint32_t kph = 0;
             const int oob_row = p.n_slots * chunk;
             int it = 0;
+            uint32_t kt_ev = 0;
             for (;; ++it) {
                 const int slot = it % kRing;
                 if (it >= kRing) mbar_wait(&s.item_empty[slot], ((it / kRing) - 1) & 1);
@@ -205,7 +222,10 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                         const int page = j * ppt + pg;
                         rows[pg] = (pg < ppt && page < np) ? __ldg(table + page) * chunk : oob_row;
                     }
+                    unsigned long long* tk = dt_trace_slot(p.trace, 3, kt_ev++);
+                    if (tk) tk[0] = dt_clk();
                     mbar_wait(&s.k_empty[stage], kph ^ 1);
+                    if (tk) tk[1] = dt_clk();
                     mbar_arrive_expect_tx(&s.k_full[stage], kStageTx);
 #pragma unroll
                     for (int pg = 0; pg < 16; ++pg)
@@ -222,6 +242,7 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
             int stage = 0;
             uint32_t vph = 0;
             const int oob_row = p.n_slots * chunk;
+            uint32_t vt_ev = 0;
             for (int it = 0;; ++it) {
                 const int slot = it % kRing;
                 mbar_wait(&s.item_full[slot], (it / kRing) & 1);
@@ -240,7 +261,10 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                         const int page = j * ppt + pg;
                         rows[pg] = (pg < ppt && page < np) ? __ldg(table + page) * chunk : oob_row;
                     }
+                    unsigned long long* tv = dt_trace_slot(p.trace, 4, vt_ev++);
+                    if (tv) tv[0] = dt_clk();
                     mbar_wait(&s.v_empty[stage], vph ^ 1);
+                    if (tv) tv[1] = dt_clk();
                     mbar_arrive_expect_tx(&s.v_full[stage], kStageTx);
 #pragma unroll
                     for (int pg = 0; pg < 16; ++pg)
@@ -292,14 +316,19 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                 tc_fence_after();
                 issue_s(qb, T);
                 for (int j = 0; j < nt; ++j, ++T) {
+                    unsigned long long* tm = dt_trace_slot(p.trace, 2, T);
+                    if (tm) tm[0] = dt_clk();
                     if (j + 1 < nt) { // S(j+1) overlaps softmax(j)
                         mbar_wait(&s.k_full[stage], kph);
                         tc_fence_after();
                         issue_s(qb, T + 1);
                     }
+                    if (tm) tm[1] = dt_clk();
                     mbar_wait(&s.p_full[T & 1], (T >> 1) & 1);
+                    if (tm) tm[2] = dt_clk();
                     if (j == 0 && it > 0) mbar_wait(&s.o_empty, (it - 1) & 1);
                     mbar_wait(&s.v_full[vstage], vph);
+                    if (tm) tm[3] = dt_clk();
                     tc_fence_after();
                     const uint64_t ad = umma_desc_sw128(smem_u32(s.v[vstage][0]), kHalf, 1024);
                     const uint64_t bd = umma_desc_sw128(smem_u32(s.pt[T & 1][0]), 16, 1024);
@@ -310,6 +339,11 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                     }
                     umma_commit(&s.pv_done[T & 1]);
                     umma_commit(&s.v_empty[vstage]);
+                    if (tm) {
+                        tm[4] = dt_clk();
+                        tm[6] = j;
+                        tm[7] = item;
+                    }
                     if (++vstage == kStages) { vstage = 0; vph ^= 1; }
                 }
                 umma_commit(&s.q_empty[qb]);
@@ -343,7 +377,10 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                 l_thr[h] = 0.f;
             }
             for (int j = 0; j < nt; ++j, ++T) {
+                unsigned long long* ts = (warp == w_sm0 && lane == 0) ? dt_trace_slot(p.trace, 0, T) : nullptr;
+                if (ts) ts[0] = dt_clk();
                 mbar_wait(&s.s_full[T & 1], (T >> 1) & 1);
+                if (ts) ts[1] = dt_clk();
                 tc_fence_after();
                 uint32_t sr[16];
                 tmem_ld16(t_lane + (T & 1) * kN, sr);
@@ -363,6 +400,7 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                     s.red[T & 1][quad][lane] = v;
                 }
                 bar_softmax();
+                if (ts) ts[2] = dt_clk();
                 bool rescale = false;
                 float corr[G];
 #pragma unroll
@@ -417,6 +455,11 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                 fence_proxy_async_smem();
                 tc_fence_before();
                 mbar_arrive(&s.p_full[T & 1]);
+                if (ts) {
+                    ts[3] = dt_clk();
+                    ts[6] = j;
+                    ts[7] = item;
+                }
             }
             // ---------------- epilogue: O^T lane r = output dim r ----------------
             mbar_wait(&s.pv_done[(T - 1) & 1], ((T - 1) >> 1) & 1);
