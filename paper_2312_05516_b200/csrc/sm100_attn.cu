@@ -86,7 +86,10 @@ constexpr bool kUseSetMaxNReg = PB_SETMAXNREG != 0;
 constexpr int kLaunchRegs = (65536 / kThreads) / 8 * 8;
 static_assert((PB_REG_HI - kLaunchRegs) * kSoftWG <= (kLaunchRegs - PB_REG_LO),
               "setmaxnreg budget exceeds the launch register allocation");
-constexpr float kRescaleThreshold = 8.0f; // log2 domain: rescale only if max grows by > 2^8
+#ifndef PB_RESCALE_THR
+#define PB_RESCALE_THR 8.0f
+#endif
+constexpr float kRescaleThreshold = PB_RESCALE_THR; // log2 domain: rescale only if max grows by > 2^thr
 #ifndef PB_ABLATE_MODE
 #define PB_ABLATE_MODE 0 // roofline ablations, separate builds only: 1 no softmax, 2 no exp2, 5 no P store
 #endif
@@ -100,11 +103,12 @@ constexpr int kPolyCols = PB_POLY_COLS;
 #define PB_POLY_EVERY 0 // exp2 of one pair in N on the FMA pipe, interleaved with the MUFU pairs
 #endif
 static_assert(kPolyCols % 32 == 0 && kPolyCols <= 64, "poly columns: whole 32-column chunks of the second P half");
-#ifndef PB_P_HALVES
-#define PB_P_HALVES 1 // 1: P released in two 64-column halves, PV of the first half overlaps the
-                      // softmax of the second
+#ifndef PB_P_PARTS
+#define PB_P_PARTS 2 // P released in this many column parts; PV of a part overlaps the softmax of
+                     // the next (1: one release per tile)
 #endif
-constexpr int kPParts = PB_P_HALVES ? 2 : 1;
+constexpr int kPParts = PB_P_PARTS;
+static_assert(kPParts == 1 || kPParts == 2 || kPParts == 4, "P parts");
 #ifndef PB_MUFU_LOCK
 #define PB_MUFU_LOCK 0 // 1: the two softmax warps of an SMSP (query tiles A, B) take turns on
                        // the MUFU pipe.  Measured slower (434 vs 418 us on the config-4 tiles):
