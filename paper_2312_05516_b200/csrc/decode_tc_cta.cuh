@@ -423,6 +423,7 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                         st_shared_u16(ptb + h * 128 + ((pt_c16 ^ (h & 7)) << 4), *reinterpret_cast<const uint16_t*>(&b));
                     }
                 }
+                if (ts) ts[4] = dt_clk();
                 if (!valid && j + 1 == nt) {
                     // rows past the unit's end in a fetched page may hold anything (stale or
                     // never-written pool rows): zero their V so 0 * NaN cannot reach O
@@ -452,12 +453,13 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                         tmem_st_wait();
                     }
                 }
+                if (ts) ts[5] = dt_clk();
                 fence_proxy_async_smem();
+                if (ts) ts[6] = dt_clk();
                 tc_fence_before();
                 mbar_arrive(&s.p_full[T & 1]);
                 if (ts) {
                     ts[3] = dt_clk();
-                    ts[6] = j;
                     ts[7] = item;
                 }
             }

@@ -44,6 +44,7 @@ def med(vals):
 
 
 for role, name, fields in ((0, "softmax", ["wait_S", "reduce", "exp_arrive"]),
+                           (0, "softmax_detail", ["wait_S", "reduce", "exp_pstore", "vzero_rescale", "fence"]),
                            (2, "mma", ["k_wait_s_issue", "p_wait", "v_wait", "pv_issue"]),
                            (3, "k_prod", ["stage_wait"]), (4, "v_prod", ["stage_wait"])):
     d = {f: [] for f in fields}
@@ -52,9 +53,11 @@ for role, name, fields in ((0, "softmax", ["wait_S", "reduce", "exp_arrive"]),
         ev = t[c, role]
         ev = ev[ev[:, 0] > 0]
         for i in range(1, len(ev)):
+            seq = [0, 1, 2, 4, 5, 6] if name == "softmax_detail" else list(range(len(fields) + 1))
             for fi, f in enumerate(fields):
-                if ev[i, fi + 1] and ev[i, fi]:
-                    d[f].append(int(ev[i, fi + 1] - ev[i, fi]))
+                a, b = seq[fi], seq[fi + 1]
+                if ev[i, b] and ev[i, a]:
+                    d[f].append(int(ev[i, b] - ev[i, a]))
             per.append(int(ev[i, 0] - ev[i - 1, 0]))
     res[name] = {f: med(vs) for f, vs in d.items()}
     res[name]["period"] = med(per)
