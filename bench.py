@@ -79,7 +79,8 @@ class ClockSampler:
     def __init__(self, index: int):
         self.index = index
         self.proc = None
-        self.lines = []
+        self.lines = []  # (arrival time, line)
+        self.t_begin = None
 
     def start(self):
         try:
@@ -93,11 +94,24 @@ class ClockSampler:
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.time(), line.strip()))
+
+    def wait_ready(self, timeout_s: float = 3.0):
+        """Block until nvidia-smi delivers its first sample (it starts slowly)."""
+        t_end = time.time() + timeout_s
+        while self.proc and not self.lines and time.time() < t_end:
+            time.sleep(0.01)
+
+    def begin(self):
+        """Mark the start of the timed region (start() runs earlier: nvidia-smi needs a few
+        hundred ms before its first sample, longer than some timed regions)."""
+        self.t_begin = time.time()
 
     def stop(self):
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        t_end = time.time()
+        time.sleep(0.03)  # the last in-window sample reaches the reader
         self.proc.terminate()
         try:
             self.proc.wait(timeout=5)
@@ -105,7 +119,9 @@ class ClockSampler:
             self.proc.kill()
         sm, mx, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        t0 = self.t_begin if self.t_begin is not None else 0.0
+        window = [ln for t, ln in self.lines if t0 <= t <= t_end + 0.02]
+        for ln in window:
             parts = [x.strip() for x in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -260,16 +276,18 @@ def measure_attention(args, cfg, n_layer, steps, warmup, rank, world, dev, with_
             dist.barrier()
         torch.cuda.synchronize()
 
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    clocks.wait_ready()
     for _ in range(warmup):
         step()
     barrier()
     # ---- timed region: K steps, per-layer events for the dominant kernel's duration ----
-    clocks = ClockSampler(dev.index)
-    clocks.start()
     n_ev = steps * n_layer
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev + 1)]
     launches0 = abi.launch_count()
     barrier()
+    clocks.begin()
     ev[0].record(stream)
     i = 0
     for _ in range(steps):
@@ -562,16 +580,18 @@ def config5_result(args, warmup):
             pl.run(q.data_ptr(), k.data_ptr() + l * layer_stride, v.data_ptr() + l * layer_stride, out.data_ptr(),
                    wsb.data_ptr(), cs.cuda_stream)
 
+    clocks = ClockSampler(dev.index)
+    clocks.start()
+    clocks.wait_ready()
     for i in range(warmup):
         run(i)
     torch.cuda.synchronize()
     t0 = torch.cuda.Event(enable_timing=True)
     t1 = torch.cuda.Event(enable_timing=True)
     swap_ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(c5_steps)]
-    clocks = ClockSampler(dev.index)
-    clocks.start()
     launches0 = abi.launch_count()
     torch.cuda.synchronize()
+    clocks.begin()
     t0.record(cs)
     for s in range(c5_steps):
         run(warmup + s, swap_ev[s])
