@@ -94,3 +94,13 @@ def test_long_contexts(gh, oracle, flags):
     convs = [[(16383, 1)], [(16000, 100)], [(5000, 1)], [(0, 300)]]
     w = _build("long", 16, 2, 128, 16, PB_BF16, 8, convs, SplitMix64(8))
     _check(gh, oracle, w, flags)
+
+
+@pytest.mark.parametrize("d,chunk", [(96, 16), (256, 16), (32, 8), (128, 24)])
+def test_shapes_outside_the_tensor_core_paths(gh, oracle, d, chunk):
+    """Head sizes other than 64 / 128 and pages that do not tile a 128-row kv tile run on the
+    SIMT kernel (bf16 in, fp32 accumulation); same contract, same oracle."""
+    convs = [[(0, 50)], [(300, 1)], [(77, 9)], [(1000, 1)]]
+    w = _build(f"simt{d}", 8, 2, d, chunk, PB_BF16, 9, convs, SplitMix64(9))
+    plan = _check(gh, oracle, w)
+    assert plan.stats()["simt_tiles"] > 0
