@@ -40,7 +40,14 @@ using namespace pb::sm100;
 constexpr int kDtThreads = 224;     // TMA K warp, MMA warp, 4 softmax warps, TMA V warp
 constexpr int kKvRows = 128;         // kv rows per tile
 constexpr int kN = 16;               // padded query heads (N of both MMAs)
-constexpr int kStages = 3;           // K/V ring depth
+#ifndef PB_DEC_K_STAGES
+#define PB_DEC_K_STAGES 3
+#endif
+#ifndef PB_DEC_V_STAGES
+#define PB_DEC_V_STAGES 3
+#endif
+constexpr int kKStages = PB_DEC_K_STAGES;  // K ring depth
+constexpr int kVStages = PB_DEC_V_STAGES;  // V ring depth
 constexpr int kRing = 4;             // work-unit ring
 constexpr uint32_t kTmemCols = 64;   // S^T buffers [0,16) [16,32), O^T [32,48)
 constexpr uint32_t kColO = 32;
@@ -49,8 +56,8 @@ constexpr uint32_t kHalf = kKvRows * 128;          // one 64-dim half of a kv ti
 constexpr uint32_t kStageTx = 2u * kHalf;          // one of K or V, two halves (D = 128)
 
 struct __align__(1024) DtSmem {
-    uint8_t k[kStages][2][kHalf];   // [stage][half][row][128 B], SW128 K-major (A of S^T)
-    uint8_t v[kStages][2][kHalf];   // same layout, read as the MN-major A of O^T
+    uint8_t k[kKStages][2][kHalf];   // [stage][half][row][128 B], SW128 K-major (A of S^T)
+    uint8_t v[kVStages][2][kHalf];   // same layout, read as the MN-major A of O^T
     uint8_t q[2][2][kN * 128];      // [unit parity][half][head][128 B], SW128 K-major (B of S^T)
     uint8_t pt[2][2][kN * 128];     // [tile parity][kv half][head][128 B], SW128 K-major (B of O^T)
     float red[2][4][kN];            // [tile parity][warp quadrant][head] max exchange
@@ -58,7 +65,7 @@ struct __align__(1024) DtSmem {
     int32_t flag;
     // separate K and V rings with their own producer warps: a K stage is free as soon as S
     // has read it, so K runs further ahead and more bytes are in flight per CTA
-    uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
+    uint64_t k_full[kKStages], k_empty[kKStages], v_full[kVStages], v_empty[kVStages];
     uint64_t q_full[2], q_empty[2];
     // p_full / pv_done per tile parity: the softmax may run one tile ahead of the MMA warp's
     // p_full wait (it no longer waits for PV(j-1) before releasing P(j)), so a single barrier
@@ -125,9 +132,11 @@ __device__ __forceinline__ int unit_tiles(const WorkItem& w, int chunk) {
 
 // thread 0 only: the decode pipeline's barriers
 __device__ __forceinline__ void decode_cta_init(DtSmem& s) {
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < kKStages; ++i) {
         mbar_init(&s.k_full[i], 1);
         mbar_init(&s.k_empty[i], 1);
+    }
+    for (int i = 0; i < kVStages; ++i) {
         mbar_init(&s.v_full[i], 1);
         mbar_init(&s.v_empty[i], 1);
     }
@@ -150,9 +159,11 @@ __device__ __forceinline__ void decode_cta_init(DtSmem& s) {
 
 // thread 0 only, pipeline drained: release the barriers' memory for another layout
 __device__ __forceinline__ void decode_cta_inval(DtSmem& s) {
-    for (int i = 0; i < kStages; ++i) {
+    for (int i = 0; i < kKStages; ++i) {
         mbar_inval(&s.k_full[i]);
         mbar_inval(&s.k_empty[i]);
+    }
+    for (int i = 0; i < kVStages; ++i) {
         mbar_inval(&s.v_full[i]);
         mbar_inval(&s.v_empty[i]);
     }
@@ -232,7 +243,7 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                         if (pg < ppt)
                             for (int h = 0; h < 2; ++h)
                                 tma_load_3d(s.k[stage][h] + pg * chunk * 128, tm_k, &s.k_full[stage], h * 64, w.kvh, rows[pg]);
-                    if (++stage == kStages) { stage = 0; kph ^= 1; }
+                    if (++stage == kKStages) { stage = 0; kph ^= 1; }
                 }
             }
         }
@@ -271,7 +282,7 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                         if (pg < ppt)
                             for (int h = 0; h < 2; ++h)
                                 tma_load_3d(s.v[stage][h] + pg * chunk * 128, tm_v, &s.v_full[stage], h * 64, w.kvh, rows[pg]);
-                    if (++stage == kStages) { stage = 0; vph ^= 1; }
+                    if (++stage == kVStages) { stage = 0; vph ^= 1; }
                 }
             }
         }
@@ -296,7 +307,7 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                 }
                 umma_commit(&s.s_full[tile & 1]);
                 umma_commit(&s.k_empty[stage]); // K is read by S only
-                if (++stage == kStages) { stage = 0; kph ^= 1; }
+                if (++stage == kKStages) { stage = 0; kph ^= 1; }
             };
             for (int it = 0;; ++it) {
                 const int slot = it % kRing;
@@ -344,7 +355,7 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                         tm[6] = j;
                         tm[7] = item;
                     }
-                    if (++vstage == kStages) { vstage = 0; vph ^= 1; }
+                    if (++vstage == kVStages) { vstage = 0; vph ^= 1; }
                 }
                 umma_commit(&s.q_empty[qb]);
             }
@@ -427,10 +438,10 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                 if (!valid && j + 1 == nt) {
                     // rows past the unit's end in a fetched page may hold anything (stale or
                     // never-written pool rows): zero their V so 0 * NaN cannot reach O
-                    const int stg = static_cast<int>(T % kStages);
+                    const int stg = static_cast<int>(T % kVStages);
                     // V arrives on its own ring: wait until this tile's V landed before zeroing
                     // (its next reuse needs PV(T), so the parity wait is exact)
-                    mbar_wait(&s.v_full[stg], (T / kStages) & 1);
+                    mbar_wait(&s.v_full[stg], (T / kVStages) & 1);
 #pragma unroll
                     for (int h = 0; h < 2; ++h)
 #pragma unroll
