@@ -266,10 +266,15 @@ def measure_attention(args, cfg, n_layer, steps, warmup, rank, world, dev, with_
     ws = torch.zeros(max(1, plan.workspace_bytes()), dtype=torch.uint8, device=dev)
     stats = plan.stats()
 
+    # the layer loop is one CUDA graph launch per step (pb_attn_run_layers: captured during
+    # the warm-up, replayed while the pointers stay the same)
+    qs = [q.data_ptr()] * n_layer
+    outs = [out.data_ptr()] * n_layer
+    kps = [x.data_ptr() for x in pools_k]
+    vps = [x.data_ptr() for x in pools_v]
+
     def step():
-        for l in range(n_layer):
-            plan.run(q.data_ptr(), pools_k[l].data_ptr(), pools_v[l].data_ptr(), out.data_ptr(),
-                     ws.data_ptr(), sh)
+        plan.run_layers(qs, kps, vps, outs, ws.data_ptr(), sh)
 
     def barrier():
         if world > 1:
@@ -282,24 +287,21 @@ def measure_attention(args, cfg, n_layer, steps, warmup, rank, world, dev, with_
     for _ in range(warmup):
         step()
     barrier()
-    # ---- timed region: K steps, per-layer events for the dominant kernel's duration ----
-    n_ev = steps * n_layer
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev + 1)]
+    # ---- timed region: K steps, an event pair around each step's graph launch; the dominant
+    # kernel's average launch duration is the step time over its n_layer launches (the one
+    # kernel per layer, back to back inside the graph, so inter-launch gaps count against it) ----
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(steps + 1)]
     launches0 = abi.launch_count()
     barrier()
     clocks.begin()
     ev[0].record(stream)
-    i = 0
-    for _ in range(steps):
-        for l in range(n_layer):
-            plan.run(q.data_ptr(), pools_k[l].data_ptr(), pools_v[l].data_ptr(), out.data_ptr(),
-                     ws.data_ptr(), sh)
-            i += 1
-            ev[i].record(stream)
+    for i in range(steps):
+        step()
+        ev[i + 1].record(stream)
     barrier()
     launches = abi.launch_count() - launches0
-    total_ms = ev[0].elapsed_time(ev[n_ev])
-    per_launch = [ev[j].elapsed_time(ev[j + 1]) for j in range(n_ev)]
+    total_ms = ev[0].elapsed_time(ev[steps])
+    per_launch = [ev[j].elapsed_time(ev[j + 1]) / n_layer for j in range(steps)]
     clk = clocks.stop()
     t = torch.tensor([total_ms], device=dev, dtype=torch.float64)
     if world > 1:

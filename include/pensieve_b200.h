@@ -131,6 +131,17 @@ pb_status pb_attn_run_append(pb_attn_plan* plan, const void* q, const void* k_ne
  * pb_attn_stage_bytes(plan) bytes).  Asynchronous on `stream`: when `stream` completes,
  * every out_host[l] is written.  Host buffers should be pinned for the copies to overlap. */
 size_t pb_attn_stage_bytes(const pb_attn_plan* plan);
+/* The layer loop on device pointers: pb_attn_run(q[l], k_pages[l], v_pages[l], out[l]) for
+ * l < n_layer, issued as ONE CUDA graph launch (the per-layer worker loop of
+ * PAPER.md:730-732; each launch replaces paged_multi_token_attention / single_token_attention,
+ * src/attention.cpp:73-188).  The graph is captured on the first call and replayed while the
+ * pointers, n_layer, workspace and trace buffer stay the same (a change re-captures it); it
+ * removes the per-launch gap between back-to-back layers.  Inside a caller's own stream
+ * capture the launches are issued directly into the caller's graph.  Same stream and
+ * workspace rules as pb_attn_run. */
+pb_status pb_attn_run_layers(pb_attn_plan* plan, int32_t n_layer, const void* const* q,
+                             const void* const* k_pages, const void* const* v_pages, void* const* out,
+                             void* workspace, void* stream);
 /* Diagnostics: when d_trace (device, >= 148 * 2 * 4 uint64) is set, the fused launch writes
  * per CTA and pass {mode (0 tile, 1 decode), items taken, begin ns, end ns}.  NULL disables. */
 void pb_attn_set_trace(pb_attn_plan* plan, void* d_trace);

@@ -117,6 +117,7 @@ _SIGS = {
     "pb_attn_run_append": (_I32, [_P, _P, _P, _P, _P, _P, _P, _P, _P]),
     "pb_attn_set_trace": (None, [_P, _P]),
     "pb_attn_run_layers_host": (_I32, [_P, _I32, _P, _P, _P, _P, _P, _P, _P]),
+    "pb_attn_run_layers": (_I32, [_P, _I32, _P, _P, _P, _P, _P, _P]),
     "pb_attn_check_numerics": (_I32, [_P, _P, _P, _P, _P]),
     "pb_attn_plan_destroy": (None, [_P]),
     "pb_paged_multi_token_attention": (_I32, [_SHP, _I32, _P, _P, _P, _P, _P, _P, _P, _I64, _P, _P, _P]),
@@ -183,6 +184,17 @@ class AttentionPlan:
                    workspace: Optional[int], stream: Optional[int] = None) -> None:
         """pb_attn_run_append: write the batch's new K/V rows into the pages, then attend."""
         check(lib.pb_attn_run_append(self._h, q, k_new, v_new, k_pages, v_pages, out, workspace, stream))
+
+    def run_layers(self, q: Sequence[int], k_pages: Sequence[int], v_pages: Sequence[int],
+                   out: Sequence[int], workspace: Optional[int], stream: Optional[int] = None) -> None:
+        """pb_attn_run_layers: the layer loop as one CUDA graph launch (captured on first use,
+        replayed while the pointers stay the same)."""
+        n = len(q)
+        if not (len(k_pages) == len(v_pages) == len(out) == n):
+            raise DimensionMismatch("per-layer pointer lists differ in length")
+        arr = ctypes.c_void_p * n
+        keep = (arr(*q), arr(*k_pages), arr(*v_pages), arr(*out))
+        check(lib.pb_attn_run_layers(self._h, n, *[ctypes.cast(a, _P) for a in keep], workspace, stream))
 
     def set_trace(self, d_trace: Optional[int]) -> None:
         lib.pb_attn_set_trace(self._h, d_trace)

@@ -16,10 +16,18 @@ namespace pb {
 namespace {
 thread_local std::string t_last_error;
 std::atomic<uint64_t> g_launches{0};
+thread_local uint64_t* t_capture_count = nullptr; // set while this thread captures a graph
 } // namespace
 
 void set_last_error(const std::string& msg) { t_last_error = msg; }
-void count_launch(uint64_t n) { g_launches.fetch_add(n, std::memory_order_relaxed); }
+void count_launch(uint64_t n) {
+    if (t_capture_count)
+        *t_capture_count += n; // captured into a graph: counted when the graph is launched
+    else
+        g_launches.fetch_add(n, std::memory_order_relaxed);
+}
+LaunchCapture::LaunchCapture() : prev_(t_capture_count) { t_capture_count = &n; }
+LaunchCapture::~LaunchCapture() { t_capture_count = prev_; }
 
 int device_sms() {
     static std::once_flag once[kMaxDevices];

@@ -68,6 +68,12 @@ struct pb_attn_plan {
     bool uploaded = false;
     void* last_workspace = nullptr;
     Sm100Cache sm100;
+    // pb_attn_run_layers: the layer loop captured once as a CUDA graph, replayed while the
+    // pointers (and trace buffer) it was captured with stay the same
+    cudaStream_t cap = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    std::vector<const void*> gkey;
+    uint64_t g_launches = 0; // kernels per replay
 };
 
 namespace {
@@ -552,6 +558,78 @@ pb_status pb_attn_run_append(pb_attn_plan* P, const void* q, const void* k_new, 
     });
 }
 
+pb_status pb_attn_run_layers(pb_attn_plan* P, int32_t n_layer, const void* const* q,
+                             const void* const* k_pages, const void* const* v_pages, void* const* out,
+                             void* workspace, void* stream) {
+    return guarded([&] {
+        if (!P) fail(PB_ERR_ERROR, "null plan");
+        if (n_layer < 0) fail(PB_ERR_DIMENSION_MISMATCH, "n_layer < 0");
+        if (!P->uploaded) fail(PB_ERR_ERROR, "plan not uploaded (call pb_attn_plan_upload)");
+        if (n_layer == 0 || P->total_tokens == 0) return;
+        if (!q || !k_pages || !v_pages || !out) fail(PB_ERR_ERROR, "null argument");
+        for (int l = 0; l < n_layer; ++l)
+            if (!q[l] || !k_pages[l] || !v_pages[l] || !out[l]) fail(PB_ERR_ERROR, "null device pointer");
+        if ((!P->tc_items.empty() || !P->decode_items.empty()) && !workspace)
+            fail(PB_ERR_ERROR, "workspace required");
+        cudaStream_t st = as_stream(stream);
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        cuda_check(cudaStreamIsCapturing(st, &cs), "capture status");
+        if (cs != cudaStreamCaptureStatusNone) {
+            // inside the caller's own capture: the launches become part of the caller's graph
+            for (int l = 0; l < n_layer; ++l) run_impl(P, q[l], k_pages[l], v_pages[l], out[l], workspace, st, nullptr, nullptr);
+            return;
+        }
+        std::vector<const void*> key;
+        key.reserve(4 * static_cast<size_t>(n_layer) + 3);
+        key.push_back(workspace);
+        key.push_back(P->trace);
+        key.push_back(reinterpret_cast<const void*>(static_cast<intptr_t>(n_layer)));
+        for (int l = 0; l < n_layer; ++l) {
+            key.push_back(q[l]);
+            key.push_back(k_pages[l]);
+            key.push_back(v_pages[l]);
+            key.push_back(out[l]);
+        }
+        if (!P->gexec || key != P->gkey) {
+            // the tickets of a new workspace are zeroed here, on the caller's stream, so the
+            // graph itself holds only the attention launches
+            if (workspace && workspace != P->last_workspace) {
+                cuda_check(cudaMemsetAsync(workspace, 0, 256, st), "workspace init");
+                P->last_workspace = workspace;
+            }
+            if (!P->cap) cuda_check(cudaStreamCreateWithFlags(&P->cap, cudaStreamNonBlocking), "capture stream");
+            if (P->gexec) {
+                cuda_check(cudaGraphExecDestroy(P->gexec), "graph destroy");
+                P->gexec = nullptr;
+                P->gkey.clear();
+            }
+            cudaGraph_t g = nullptr;
+            uint64_t n_launch = 0;
+            cuda_check(cudaStreamBeginCapture(P->cap, cudaStreamCaptureModeRelaxed), "begin capture");
+            try {
+                LaunchCapture counted;
+                for (int l = 0; l < n_layer; ++l)
+                    run_impl(P, q[l], k_pages[l], v_pages[l], out[l], workspace, P->cap, nullptr, nullptr);
+                n_launch = counted.n;
+            } catch (...) {
+                cudaStreamEndCapture(P->cap, &g);
+                if (g) cudaGraphDestroy(g);
+                throw;
+            }
+            cuda_check(cudaStreamEndCapture(P->cap, &g), "end capture");
+            cudaGraphExec_t ge = nullptr;
+            const cudaError_t e = cudaGraphInstantiate(&ge, g, 0);
+            cudaGraphDestroy(g);
+            cuda_check(e, "graph instantiate");
+            P->gexec = ge;
+            P->gkey = std::move(key);
+            P->g_launches = n_launch;
+        }
+        cuda_check(cudaGraphLaunch(P->gexec, st), "graph launch");
+        count_launch(P->g_launches);
+    });
+}
+
 void pb_attn_set_trace(pb_attn_plan* P, void* d_trace) {
     if (P) P->trace = d_trace;
 }
@@ -643,6 +721,8 @@ void pb_attn_plan_destroy(pb_attn_plan* P) {
         cudaEventDestroy(P->fork);
         cudaEventDestroy(P->join);
     }
+    if (P->gexec) cudaGraphExecDestroy(P->gexec);
+    if (P->cap) cudaStreamDestroy(P->cap);
     delete P;
 }
 

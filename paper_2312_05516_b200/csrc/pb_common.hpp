@@ -29,6 +29,18 @@ inline void require(bool ok, const char* what) {
 
 void set_last_error(const std::string& msg);
 void count_launch(uint64_t n = 1);
+// While alive, this thread's count_launch calls add to `n` instead of the process counter
+// (kernels captured into a graph are counted per graph launch).
+struct LaunchCapture {
+    uint64_t n = 0;
+    LaunchCapture();
+    ~LaunchCapture();
+    LaunchCapture(const LaunchCapture&) = delete;
+    LaunchCapture& operator=(const LaunchCapture&) = delete;
+
+  private:
+    uint64_t* prev_;
+};
 
 inline void cuda_check(cudaError_t e, const char* what) {
     if (e != cudaSuccess)

@@ -118,3 +118,14 @@ def test_work_list_covers_every_row():
     for force in (abi.PB_PLAN_FORCE_SIMT, abi.PB_PLAN_NO_SPLIT):
         st2 = AttentionPlan(w.shape(), w.batch(), flags=force).stats()
         assert st2["rows"] == w.total_tokens * w.n_head
+
+
+def test_run_layers_checks_arguments_before_any_device_call():
+    """pb_attn_run_layers rejects a plan that was never uploaded and mismatched per-layer
+    lists before touching the device (its run_impl checks, in the same order)."""
+    w = config(2)
+    plan = AttentionPlan(w.shape(), w.batch())
+    with pytest.raises(abi.Error):
+        plan.run_layers([1, 1], [1, 1], [1, 1], [1, 1], 1, None)
+    with pytest.raises(abi.DimensionMismatch):
+        plan.run_layers([1, 1], [1], [1, 1], [1, 1], 1, None)
