@@ -7,7 +7,7 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 from paper_2312_05516_b200 import abi  # noqa: E402
-from paper_2312_05516_b200.abi import PB_BF16, AttentionPlan  # noqa: E402
+from paper_2312_05516_b200.abi import PB_BF16, PB_F32, AttentionPlan  # noqa: E402
 from paper_2312_05516_b200.workloads import SplitMix64, random_instance  # noqa: E402
 
 L = 4
@@ -42,10 +42,13 @@ def _same(torch, a, b):
     return all(torch.equal(x.view(torch.int16), y.view(torch.int16)) for x, y in zip(a, b))
 
 
-@pytest.mark.parametrize("flags", [0, abi.PB_PLAN_SEPARATE_DECODE])
-def test_graph_layers_equal_eager_layers(gh, cuda, flags):
+@pytest.mark.parametrize("flags,d,dtype", [(0, 128, PB_BF16), (abi.PB_PLAN_SEPARATE_DECODE, 128, PB_BF16),
+                                           (0, 64, PB_BF16), (0, 128, PB_F32)])
+def test_graph_layers_equal_eager_layers(gh, cuda, flags, d, dtype):
+    """bf16 d = 128 (fused and separate schedules), d = 64, and the fp32 validation mode (SIMT
+    kernels) inside the graph."""
     torch = cuda
-    w = random_instance(SplitMix64(77), 32, 4, 128, 16, PB_BF16, 10, 2500, max_q=300)
+    w = random_instance(SplitMix64(77), 32, 4, d, 16, dtype, 10, 2500, max_q=300)
     q, ks, vs = _layers(gh, w)
     st = torch.cuda.current_stream().cuda_stream
     plan = AttentionPlan(w.shape(), w.batch(), flags)
@@ -69,7 +72,7 @@ def test_graph_layers_equal_eager_layers(gh, cuda, flags):
     assert abi.launch_count() - n0 == 2 * per_call
 
     # the graph reads the pools when it runs: new contents, same pointers
-    abi.fill_unit(ks[1].data_ptr(), PB_BF16, w.pool_elems, w.seed + 1, 0)
+    abi.fill_unit(ks[1].data_ptr(), dtype, w.pool_elems, w.seed + 1, 0)
     want2 = _eager(torch, plan, q, ks, vs, ws, st)
     plan.run_layers(*args, ws.data_ptr(), st)
     torch.cuda.synchronize()
