@@ -78,6 +78,18 @@ struct __align__(1024) DtSmem {
 };
 
 __device__ __forceinline__ void bar_softmax() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+// bar_softmax with an OR-reduction of one predicate over the four softmax warps
+__device__ __forceinline__ bool bar_softmax_any(bool v) {
+    uint32_t r;
+    asm volatile("{\n\t.reg .pred pi, po;\n\t"
+                 "setp.ne.u32 pi, %1, 0;\n\t"
+                 "bar.red.or.pred po, 1, 128, pi;\n\t"
+                 "selp.u32 %0, 1, 0, po;\n\t}"
+                 : "=r"(r)
+                 : "r"(static_cast<uint32_t>(v))
+                 : "memory");
+    return r != 0;
+}
 
 #ifndef PB_TILE_TRACE
 #define PB_TILE_TRACE 0
@@ -404,26 +416,36 @@ __device__ __forceinline__ void decode_cta_run(DtSmem& s, const uint32_t tmem, c
                     x[h] = (valid && h < g) ? __uint_as_float(sr[h]) * sl2 : -CUDART_INF_F;
                     mt[h] = warp_max_f32(x[h]);
                 }
-                if (lane < G) {
-                    float v = mt[0];
+                // The heads' maxima over the tile only matter when one grows past the lazy
+                // threshold: a barrier OR-reduction asks whether any warp sees that; usually
+                // none does and the 4-warp exchange is skipped (same results either way).
+                bool want = false;
 #pragma unroll
-                    for (int h = 1; h < G; ++h) v = lane == h ? mt[h] : v;
-                    s.red[T & 1][quad][lane] = v;
-                }
-                bar_softmax();
-                if (ts) ts[2] = dt_clk();
+                for (int h = 0; h < G; ++h) want |= mt[h] > m_run[h] + kThr;
                 bool rescale = false;
                 float corr[G];
 #pragma unroll
-                for (int h = 0; h < G; ++h) {
-                    const float m4 = fmaxf(fmaxf(s.red[T & 1][0][h], s.red[T & 1][1][h]),
-                                           fmaxf(s.red[T & 1][2][h], s.red[T & 1][3][h]));
-                    const bool grow = m4 > m_run[h] + kThr; // uniform across the 128 threads
-                    const float m_new = grow ? m4 : m_run[h];
-                    corr[h] = grow ? ex2(m_run[h] - m_new) : 1.f;
-                    rescale |= grow && j > 0;
-                    m_run[h] = m_new;
+                for (int h = 0; h < G; ++h) corr[h] = 1.f;
+                if (bar_softmax_any(want)) {
+                    if (lane < G) {
+                        float v = mt[0];
+#pragma unroll
+                        for (int h = 1; h < G; ++h) v = lane == h ? mt[h] : v;
+                        s.red[T & 1][quad][lane] = v;
+                    }
+                    bar_softmax();
+#pragma unroll
+                    for (int h = 0; h < G; ++h) {
+                        const float m4 = fmaxf(fmaxf(s.red[T & 1][0][h], s.red[T & 1][1][h]),
+                                               fmaxf(s.red[T & 1][2][h], s.red[T & 1][3][h]));
+                        const bool grow = m4 > m_run[h] + kThr; // uniform across the 128 threads
+                        const float m_new = grow ? m4 : m_run[h];
+                        corr[h] = grow ? ex2(m_run[h] - m_new) : 1.f;
+                        rescale |= grow && j > 0;
+                        m_run[h] = m_new;
+                    }
                 }
+                if (ts) ts[2] = dt_clk();
                 const uint32_t ptb = smem_u32(s.pt[T & 1][0]) + pt_row;
 #pragma unroll
                 for (int h = 0; h < G; ++h) {
